@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Benchmark driver (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): the LLaMA-2-7B-shaped decoder layer stack
+(32 blocks x {q,k,v,o: 4096x4096; up,gate: 11008x4096; down: 4096x11008}),
+4-bit QEFT, g=128, k=128 weak columns, decode GEMV at batch 1. One step = one
+decode token through all 224 quantized linears, replayed as a CUDA graph.
+Weights are synthetic, directly in the B200 tile layout, 3.70 GB per step
+(far above the 126 MB L2, so no flush is needed between steps).
+
+  value     algorithmic HBM GB/s of the stack, device-timed (CUDA events),
+            max over ranks, summed over ranks (replicas: decode does not shard)
+  e2e       same metric through the public API LinearStack.run(): pinned host
+            x -> device, graph replay, all outputs -> pinned host, wall clock
+  roofline  dominant GEMV shape timed alone with CUDA events, algorithmic bytes
+            per launch / mean launch time vs MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the CPU oracle (numpy port of pkg/src/qeft/kernels.py
+            matvec_structured) on one decoder block, rank 0, N=1
+
+`--impl reference` times the reference algorithm on the host CPU (the oracle
+port; the numpy reference cannot travel to the GPU box) on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "QEFT decode GEMV HBM GB/s (% peak); fine-tune tokens/s at 1/2/4/8 B200"
+WORKLOAD = ("LLaMA-2-7B-shaped decoder layer stack (32 blocks x 7 linears = 224 GEMVs), "
+            "4-bit QEFT g=128 k=128, decode GEMV batch 1")
+BLOCK_SHAPES = [(4096, 4096), (4096, 4096), (4096, 4096), (4096, 4096),
+                (11008, 4096), (11008, 4096), (4096, 11008)]
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_oracle_sample(seconds: float = 10.0, seed: int = 0):
+    """Time the CPU oracle's matvec_structured over one synthetic 7B decoder block
+    (7 layers, 4-bit g128 k128) until `seconds` elapse. Returns (GB/s, sample desc, cores)."""
+    from oracle import qeft_oracle as O
+    rng = np.random.default_rng(seed)
+    layers = []
+    for oc, ic in BLOCK_SHAPES:
+        k, g, m = 128, 128, ic - 128
+        packed = rng.integers(0, 256, size=oc * O.row_bytes(m, 4), dtype=np.uint8).tobytes()
+        ng = O.n_groups(m, g)
+        sc = (1e-3 + 0.01 * np.abs(rng.standard_normal((oc, ng)))).astype(np.float32)
+        zr = (0.05 * rng.standard_normal((oc, ng))).astype(np.float32)
+        weak = (0.02 * rng.standard_normal((oc, k))).astype(np.float32)
+        layers.append(O.OracleLayer(oc=oc, ic=ic, k=k, bits=4, g=g, packed=packed, scales=sc,
+                                    zeros=zr, weak=weak, weak_indices=np.arange(m, ic),
+                                    layout="structured"))
+    xs = {ic: rng.standard_normal(ic).astype(np.float32) for _, ic in BLOCK_SHAPES}
+    nbytes = [O.row_bytes(q.m, 4) * q.oc + 4 * q.oc * q.n_groups + 2 * q.oc * q.k
+              + 2 * (q.ic + q.oc) for q in layers]
+    O.matvec_structured(layers[0], xs[layers[0].ic])  # warm
+    done_b, calls, t0 = 0, 0, time.perf_counter()
+    while True:
+        for q, b in zip(layers, nbytes):
+            O.matvec_structured(q, xs[q.ic])
+            done_b += b
+            calls += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    dt = time.perf_counter() - t0
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    return done_b / dt / 1e9, f"{calls} matvec_structured calls over one 7B decoder block (7 layers), {dt:.1f} s", cores
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU algorithm (oracle port) on host cores."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    from oracle import qeft_oracle as O  # noqa: F401
+    per_step = []
+    for i in range(args.warmup + args.steps):
+        gbs, sample, cores = cpu_oracle_sample(seconds=2.0, seed=i)
+        if i >= args.warmup:
+            per_step.append(gbs)
+    v = float(statistics.mean(per_step))
+    line = {"metric": METRIC, "value": v, "unit": "GB/s", "impl": "reference", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n_cols": 1},
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "port",
+                             "sample": "per step: " + sample},
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _time_graph(fn, iters, torch):
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    for _ in range(iters):
+        fn()
+    e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3
+
+
+def kernel_roofline(torch, n_blocks, peak, n_cols):
+    """Per-shape GEMV launch time (CUDA events on the launching stream, graph of the
+    32 same-shape layers so weights stream from HBM). Returns per-shape table."""
+    from paper_2410_08661_b200.decode import LinearStack, random_layer
+    out = []
+    for si, (oc, ic) in enumerate(sorted(set(BLOCK_SHAPES))):
+        layers = [random_layer(oc, ic, 128, 4, 128, "f16", seed=9000 + si * 100 + b)
+                  for b in range(n_blocks)]
+        st = LinearStack(layers, n_cols=n_cols)
+        for _ in range(3):
+            st.step()
+        reps = 20
+        t = _time_graph(st.step, reps, torch)
+        per_launch = t / (reps * len(layers))
+        nb = st.bytes_per_step() / len(layers)
+        out.append({"shape": [oc, ic], "us_per_launch": per_launch * 1e6, "bytes_per_launch": nb,
+                    "achieved_gbs": nb / per_launch / 1e9, "frac": nb / per_launch / 1e9 / peak})
+        del st, layers
+    return out
+
+
+def run_b200(args):
+    import torch
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2410_08661_b200.decode import LinearStack, llama_stack_layers
+    peak, peak_kind = _peaks()
+    n = args.n_cols
+
+    layers = llama_stack_layers("7b", k=128, bits=4, g=128, dtype="f16", n_blocks=args.blocks)
+    stack = LinearStack(layers, n_cols=n)
+    for _ in range(args.warmup):
+        stack.step()
+    bytes_step = stack.bytes_per_step()
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            stack.step()
+        e1.record()
+        torch.cuda.synchronize()
+        # keep the GPU busy while the sampler collects enough samples
+        t_extra = time.perf_counter()
+        while time.perf_counter() - t_extra < 1.0:
+            stack.step()
+        torch.cuda.synchronize()
+    barrier()
+    t = e0.elapsed_time(e1) / 1e3
+    if ws > 1:
+        tt = torch.tensor([t], device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t = float(tt.item())
+    value = ws * bytes_step * args.steps / t / 1e9
+
+    # e2e through the public API with pinned host buffers
+    xh = {ic: torch.randn(n, ic).half() for ic in stack.ics}
+    for _ in range(2):
+        stack.run(xh)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        stack.run(xh)
+    te = time.perf_counter() - t0
+    if ws > 1:
+        tt = torch.tensor([te], device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        te = float(tt.item())
+    e2e = ws * bytes_step * args.steps / te / 1e9
+
+    roof = kernel_roofline(torch, min(args.blocks, 32), peak, n) if rank == 0 else []
+    del stack, layers
+    line = None
+    if rank == 0:
+        dom = max(roof, key=lambda r: r["us_per_launch"] * (3 if r["shape"] == [4096, 4096] else 2))
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "gemv_traffic.json")
+        if os.path.exists(tp):
+            tj = json.load(open(tp))
+            traffic = tj.get("%dx%d" % tuple(dom["shape"]))
+        cpu = None
+        if ws == 1 and not args.no_cpu:
+            gbs, sample, cores = cpu_oracle_sample(seconds=args.cpu_seconds)
+            cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample}
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n_cols": n, "blocks": args.blocks,
+                       "gemv_per_step": len(layers), "bytes_per_step": bytes_step,
+                       "l2": "inputs larger than L2 (%.2f GB of weights per step)" % (bytes_step / 1e9),
+                       "parallelism": f"replicas{ws}"},
+            "frac_of_peak": value / ws / peak, "peak_gbs": peak, "peak_kind": peak_kind,
+            "roofline": {"bound": "hbm", "achieved": dom["achieved_gbs"], "peak": peak,
+                         "unit": "GB/s", "frac": dom["frac"], "traffic": traffic,
+                         "kernel": "qeft gemv_kernel<4,1,half,FOLD> %dx%d" % tuple(dom["shape"]),
+                         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                         "per_shape": roof},
+            "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": len(layers) * args.steps,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        line["e2e"]["h2d_bytes_per_step"] = sum(2 * n * ic for ic in sorted({s[1] for s in BLOCK_SHAPES}))
+        line["e2e"]["d2h_bytes_per_step"] = sum(2 * n * oc for oc, _ in BLOCK_SHAPES) * args.blocks
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n-cols", type=int, default=1)
+    ap.add_argument("--blocks", type=int, default=32)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,144 @@
+/*
+ * qeft_b200.h — C ABI of the B200-native QEFT structured mixed-precision
+ * linear layer (arXiv 2410.08661). Built as libqeft_b200.so for sm_100a.
+ *
+ * This is the drop-in boundary for the reference package's hot path
+ * (/root/reference/pkg/src/qeft). Each entry point names the reference
+ * function it replaces. Conventions:
+ *   - all pointers are DEVICE pointers unless stated; the caller owns all
+ *     memory and the library never allocates (workspace is passed in);
+ *   - calls are stream-ordered on `stream` (a cudaStream_t, NULL = legacy);
+ *   - return 0 on success, QEFT_ERR_SHAPE (1) for shape/argument errors
+ *     (the reference raises qeft.errors.ShapeError, errors.py:16-17),
+ *     QEFT_ERR_LAYOUT (2) for unsupported layouts, QEFT_ERR_CUDA (3) for
+ *     CUDA failures; qeft_last_error() returns a thread-local message.
+ *   - activations are row-major [rows][ld] in fp16 or bf16 (act_dtype):
+ *     the torch orientation. The reference's (channels, tokens) arrays are the
+ *     transpose; the host adapter converts.
+ */
+#ifndef QEFT_B200_H
+#define QEFT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QEFT_OK 0
+#define QEFT_ERR_SHAPE 1
+#define QEFT_ERR_LAYOUT 2
+#define QEFT_ERR_CUDA 3
+
+#define QEFT_F16 0
+#define QEFT_BF16 1
+
+/* flags */
+#define QEFT_FLAG_STRUCTURED_FAST 1 /* colmap == identity-with-gap, m%8==0, ic%8==0 */
+
+/*
+ * One quantized linear layer in the B200 tile layout (see csrc/qeft_common.cuh).
+ * Field meaning follows QuantizedLinear (pkg/src/qeft/quantizer.py:42-65):
+ * m = ic - k quantized columns in groups of g (last group ragged), ng groups.
+ */
+typedef struct qeft_linear {
+  int32_t oc, ic, k, bits, g;
+  int32_t m, ng;
+  int32_t m_pad;   /* roundup(m, 128) */
+  int32_t k_pad;   /* roundup(k, 64), 0 when k == 0 */
+  int32_t oc_pad;  /* roundup(oc, 16) */
+  int32_t act_dtype; /* QEFT_F16 / QEFT_BF16: dtype of sz, weak16, activations */
+  int32_t flags;
+  const void* qweight;   /* tile-layout codes, (oc_pad/16) * rowblock bytes */
+  const void* sz;        /* (scale, zero) pairs [oc_pad/16][ng][16][2] */
+  const void* weak16;    /* [oc_pad][k_pad] */
+  const int32_t* colmap; /* [m_pad + k_pad]: B200 K position -> input column, -1 pad */
+} qeft_linear_t;
+
+/* ---- format conversion (packing.py:24-72, quantizer.py:42-100) ---- */
+
+/* Bytes of the tile-layout qweight for (oc, m, bits). */
+size_t qeft_qweight_bytes(int oc, int m, int bits);
+
+/* Reference packed bytes (pack_codes output, packing.py:24-52) -> tiles. */
+int qeft_repack_to_tiles(const uint8_t* ref_packed, int oc, int m, int bits, void* qweight,
+                         void* stream);
+/* Tiles -> reference packed bytes, bit-exact inverse (unpack/pack round trip). */
+int qeft_repack_to_ref(const void* qweight, int oc, int m, int bits, uint8_t* ref_packed,
+                       void* stream);
+/* fp32 scales/zeros [oc][ng] (quantizer.py:50-51) -> sz pairs in act_dtype. */
+int qeft_pack_sz(const float* scales, const float* zeros, int oc, int ng, int act_dtype, void* sz,
+                 void* stream);
+/* fp32 weak block [oc][k] (quantizer.py:52) -> weak16 [oc_pad][k_pad]. */
+int qeft_pack_weak(const float* weak, int oc, int k, int act_dtype, void* weak16, void* stream);
+/* QuantizedLinear.dequant_full (quantizer.py:95-100) of the device layer, fp32 [oc][ic]. */
+int qeft_dequant_full(const qeft_linear_t* layer, float* out, void* stream);
+/* xb[r][j] = x[r][colmap[j]] (0 for padding): input gather for irregular /
+ * online-reorder layers (kernels.py:110, kernels.py:123-124). */
+int qeft_gather_cols(const void* x, int64_t ldx, const int32_t* colmap, int kk, int rows,
+                     int act_dtype, void* xb, void* stream);
+
+/* ---- offline quantization (quantizer.py:115-218): RTN min-max params + nearest codes ---- */
+/* w_dense [oc][m] fp32 (already split to quantized columns). Outputs fp32 scales/zeros
+ * [oc][ng] and uint8 codes [oc][m]; bit-exact with _minmax_params/_nearest_codes. */
+int qeft_quantize_rtn(const float* w_dense, int oc, int m, int g, int bits, float* scales,
+                      float* zeros, uint8_t* codes, void* stream);
+
+/* ---- decode GEMV (kernels.py:87-157 matvec_structured/irregular/online) ----
+ * y[n][o] = sum_i W_hat[o][i] * x[n][i] for n < n_cols (1..16), x/y row-major.
+ * y is act_dtype, or fp32 when y_f32 != 0. Needs qeft_gemv_workspace_bytes()
+ * of zero-initialised workspace (kernels leave it zeroed for the next call). */
+size_t qeft_gemv_workspace_bytes(const qeft_linear_t* layer, int n_cols);
+int qeft_gemv(const qeft_linear_t* layer, const void* x, int64_t ldx, void* y, int64_t ldy, int y_f32,
+              int n_cols, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- prefill / fine-tune GEMMs on tcgen05 (tuning.py:52-103) ----
+ * fwd:   y[t][o]  = sum_i W_hat[o][i] x[t][i]                       (qlinear_forward_train)
+ * dgrad: dx[t][i] = sum_o W_hat[o][i] dy[t][o]  (+= if accumulate)  (qlinear_backward dX)
+ * wgrad: dw[o][j] (+)= sum_t dy[t][o] x[t][weak_j]   fp32 out       (qlinear_backward dW_weak)
+ * workspace: qeft_gemm_workspace_bytes() (gather buffer for non-fast layouts). */
+size_t qeft_gemm_workspace_bytes(const qeft_linear_t* layer, int T);
+int qeft_gemm_fwd(const qeft_linear_t* layer, const void* x, int64_t ldx, void* y, int64_t ldy,
+                  int T, void* workspace, size_t workspace_bytes, void* stream);
+int qeft_gemm_dgrad(const qeft_linear_t* layer, const void* dy, int64_t lddy, void* dx,
+                    int64_t lddx, int T, int accumulate, void* workspace, size_t workspace_bytes,
+                    void* stream);
+int qeft_gemm_wgrad(const qeft_linear_t* layer, const void* dy, int64_t lddy, const void* x,
+                    int64_t ldx, float* dw, int T, int accumulate, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/* ---- optimizer (tuning.py:137-160 adam_step, tuning.py:226-236 clip) ---- */
+/* out[0] = sum(g^2) in fp64 (deterministic two-pass). scratch >= 4096 doubles. */
+int qeft_grad_sqnorm(const float* g, int64_t n, double* scratch, double* out, void* stream);
+/* g /= divisor in fp32 (the reference's acc[name] /= grad_accum, tuning.py:228). */
+int qeft_div_scalar(float* g, int64_t n, float divisor, void* stream);
+/* Fused clip + Adam over a flat fp32 bucket, in place on w32/m/v.
+ * sqnorm: device fp64 from qeft_grad_sqnorm. If it is non-finite nothing is
+ * updated and *nonfinite_flag (device int) is set to 1 (DivergenceError).
+ * Constants are fp32 images of the reference's Python scalars:
+ * c_b1 = f32(b1), c_1mb1 = f32(1-b1), c_b2, c_1mb2, bc1 = f32(1-b1**t),
+ * bc2 = f32(1-b2**t). max_norm <= 0 disables clipping. */
+int qeft_adam_clip(float* w32, float* m, float* v, const float* g, int64_t n, const double* sqnorm,
+                   float max_norm, float lr, float c_b1, float c_1mb1, float c_b2, float c_1mb2,
+                   float bc1, float bc2, float eps, int* nonfinite_flag, void* stream);
+/* Refresh the weak16 shadows from the fp32 masters after the update.
+ * descs: device array of n_layers {int64 offset, int32 oc, k, k_pad, dtype, ptr}. */
+typedef struct qeft_shadow_desc {
+  int64_t offset; /* element offset of the layer's [oc][k] master in w32 */
+  int32_t oc, k, k_pad, act_dtype;
+  void* weak16;
+} qeft_shadow_desc_t;
+int qeft_weak_shadow(const float* w32, const qeft_shadow_desc_t* descs, int n_layers, int max_elems,
+                     void* stream);
+
+/* Thread-local message for the last non-zero return. */
+const char* qeft_last_error(void);
+/* Library build string (arch, version). */
+const char* qeft_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QEFT_B200_H */

@@ -1,0 +1,128 @@
+// extern "C" boundary of libqeft_b200.so (declared in include/qeft_b200.h).
+// Thin argument validation + error mapping over the kernels in this directory.
+#include <stdarg.h>
+#include <string.h>
+
+#include "qeft_common.cuh"
+#include "qeft_internal.h"
+
+namespace qeft {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+static int check_layer(const qeft_linear_t* L) {
+  QEFT_CHECK(L != nullptr, QEFT_ERR_SHAPE, "null layer");
+  QEFT_CHECK(L->bits == 3 || L->bits == 4, QEFT_ERR_SHAPE, "bits must be 3 or 4, got %d", L->bits);
+  QEFT_CHECK(L->k >= 0 && L->k < L->ic, QEFT_ERR_SHAPE, "k=%d must be < IC=%d", L->k, L->ic);
+  QEFT_CHECK(L->m == L->ic - L->k, QEFT_ERR_SHAPE, "m=%d != ic-k", L->m);
+  QEFT_CHECK(L->g >= 1 && L->ng == (L->m + L->g - 1) / L->g, QEFT_ERR_SHAPE, "bad g/ng");
+  QEFT_CHECK(L->m_pad == pad_to(L->m, 128) && L->k_pad == pad_to(L->k, 64) &&
+                 L->oc_pad == pad_to(L->oc, 16),
+             QEFT_ERR_SHAPE, "bad padding fields");
+  QEFT_CHECK(L->act_dtype == QEFT_F16 || L->act_dtype == QEFT_BF16, QEFT_ERR_SHAPE, "bad dtype");
+  return 0;
+}
+
+}  // namespace qeft
+
+using namespace qeft;
+
+#define ST(s) ((cudaStream_t)(s))
+
+extern "C" {
+
+const char* qeft_last_error(void) { return qeft::g_err; }
+
+const char* qeft_version(void) { return "qeft_b200 0.1 sm_100a"; }
+
+size_t qeft_qweight_bytes(int oc, int m, int bits) {
+  return (size_t)(pad_to(oc, 16) / 16) * (size_t)rowblock_bytes(bits, pad_to(m, 128));
+}
+
+int qeft_repack_to_tiles(const uint8_t* ref, int oc, int m, int bits, void* qw, void* s) {
+  QEFT_CHECK(bits == 3 || bits == 4, QEFT_ERR_SHAPE, "unsupported bit width %d", bits);
+  QEFT_CHECK(oc >= 0 && m >= 0, QEFT_ERR_SHAPE, "negative shape");
+  return repack_ref_to_tiles(ref, oc, m, bits, qw, ST(s));
+}
+
+int qeft_repack_to_ref(const void* qw, int oc, int m, int bits, uint8_t* ref, void* s) {
+  QEFT_CHECK(bits == 3 || bits == 4, QEFT_ERR_SHAPE, "unsupported bit width %d", bits);
+  return repack_tiles_to_ref(qw, oc, m, bits, ref, ST(s));
+}
+
+int qeft_pack_sz(const float* sc, const float* zr, int oc, int ng, int dt, void* out, void* s) {
+  return pack_sz(sc, zr, oc, ng, dt, out, ST(s));
+}
+
+int qeft_pack_weak(const float* w, int oc, int k, int dt, void* out, void* s) {
+  return pack_weak(w, oc, k, dt, out, ST(s));
+}
+
+int qeft_dequant_full(const qeft_linear_t* L, float* out, void* s) {
+  if (int r = check_layer(L)) return r;
+  return dequant_full(L, out, ST(s));
+}
+
+int qeft_gather_cols(const void* x, int64_t ldx, const int32_t* colmap, int kk, int rows, int dt,
+                     void* xb, void* s) {
+  return gather_cols(x, ldx, colmap, kk, rows, dt, xb, ST(s));
+}
+
+int qeft_quantize_rtn(const float* w, int oc, int m, int g, int bits, float* sc, float* zr,
+                      uint8_t* codes, void* s) {
+  return quantize_rtn(w, oc, m, g, bits, sc, zr, codes, ST(s));
+}
+
+size_t qeft_gemv_workspace_bytes(const qeft_linear_t* L, int n) { return gemv_workspace_bytes(L, n); }
+
+int qeft_gemv(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ldy, int y_f32,
+              int n, void* ws, size_t wsb, void* s) {
+  if (int r = check_layer(L)) return r;
+  return gemv(L, x, ldx, y, ldy, y_f32, n, ws, wsb, ST(s));
+}
+
+size_t qeft_gemm_workspace_bytes(const qeft_linear_t* L, int T) { return gemm_workspace_bytes(L, T); }
+
+int qeft_gemm_fwd(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ldy, int T,
+                  void* ws, size_t wsb, void* s) {
+  if (int r = check_layer(L)) return r;
+  return gemm_fwd(L, x, ldx, y, ldy, T, ws, wsb, ST(s));
+}
+
+int qeft_gemm_dgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, void* dx, int64_t lddx,
+                    int T, int acc, void* ws, size_t wsb, void* s) {
+  if (int r = check_layer(L)) return r;
+  return gemm_dgrad(L, dy, lddy, dx, lddx, T, acc, ws, wsb, ST(s));
+}
+
+int qeft_gemm_wgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, const void* x, int64_t ldx,
+                    float* dw, int T, int acc, void* ws, size_t wsb, void* s) {
+  if (int r = check_layer(L)) return r;
+  return gemm_wgrad(L, dy, lddy, x, ldx, dw, T, acc, ws, wsb, ST(s));
+}
+
+int qeft_grad_sqnorm(const float* g, int64_t n, double* scratch, double* out, void* s) {
+  return grad_sqnorm(g, n, scratch, out, ST(s));
+}
+
+int qeft_div_scalar(float* g, int64_t n, float d, void* s) { return div_scalar(g, n, d, ST(s)); }
+
+int qeft_adam_clip(float* w, float* m, float* v, const float* g, int64_t n, const double* sq,
+                   float max_norm, float lr, float c_b1, float c_1mb1, float c_b2, float c_1mb2,
+                   float bc1, float bc2, float eps, int* flag, void* s) {
+  return adam_clip(w, m, v, g, n, sq, max_norm, lr, c_b1, c_1mb1, c_b2, c_1mb2, bc1, bc2, eps, flag,
+                   ST(s));
+}
+
+int qeft_weak_shadow(const float* w32, const qeft_shadow_desc_t* d, int n, int max_elems, void* s) {
+  return weak_shadow(w32, d, n, max_elems, ST(s));
+}
+
+}  // extern "C"

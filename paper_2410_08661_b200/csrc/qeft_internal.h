@@ -1,0 +1,64 @@
+// Internal host-side helpers shared by the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string>
+
+#include "../../include/qeft_b200.h"
+
+namespace qeft {
+
+void set_error(const char* fmt, ...);
+
+inline int pad_to(int x, int a) { return (x + a - 1) / a * a; }
+
+#define QEFT_CUDA(expr)                                                              \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess) {                                                         \
+      ::qeft::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+      return QEFT_ERR_CUDA;                                                          \
+    }                                                                                \
+  } while (0)
+
+#define QEFT_CHECK(cond, code, ...)      \
+  do {                                   \
+    if (!(cond)) {                       \
+      ::qeft::set_error(__VA_ARGS__);    \
+      return code;                       \
+    }                                    \
+  } while (0)
+
+int repack_ref_to_tiles(const uint8_t* ref, int oc, int m, int bits, void* qw, cudaStream_t st);
+int repack_tiles_to_ref(const void* qw, int oc, int m, int bits, uint8_t* ref, cudaStream_t st);
+int pack_sz(const float* s, const float* z, int oc, int ng, int dtype, void* out, cudaStream_t st);
+int pack_weak(const float* w, int oc, int k, int dtype, void* out, cudaStream_t st);
+int dequant_full(const qeft_linear_t* L, float* out, cudaStream_t st);
+int gather_cols(const void* x, int64_t ldx, const int* colmap, int kk, int rows, int dtype, void* xb,
+                cudaStream_t st);
+int quantize_rtn(const float* w, int oc, int m, int g, int bits, float* s, float* z, uint8_t* codes,
+                 cudaStream_t st);
+
+size_t gemv_workspace_bytes(const qeft_linear_t* L, int n);
+int gemv(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ldy, int y_f32, int n,
+         void* ws, size_t ws_bytes, cudaStream_t st);
+
+size_t gemm_workspace_bytes(const qeft_linear_t* L, int T);
+int gemm_fwd(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ldy, int T,
+             void* ws, size_t ws_bytes, cudaStream_t st);
+int gemm_dgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, void* dx, int64_t lddx, int T,
+               int accumulate, void* ws, size_t ws_bytes, cudaStream_t st);
+int gemm_wgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, const void* x, int64_t ldx,
+               float* dw, int T, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st);
+
+int grad_sqnorm(const float* g, int64_t n, double* scratch, double* out, cudaStream_t st);
+int div_scalar(float* g, int64_t n, float d, cudaStream_t st);
+int adam_clip(float* w, float* m, float* v, const float* g, int64_t n, const double* sqnorm,
+              float max_norm, float lr, float c_b1, float c_1mb1, float c_b2, float c_1mb2, float bc1,
+              float bc2, float eps, int* flag, cudaStream_t st);
+int weak_shadow(const float* w32, const qeft_shadow_desc_t* d, int n_layers, int max_elems,
+                cudaStream_t st);
+
+}  // namespace qeft

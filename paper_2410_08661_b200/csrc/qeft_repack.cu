@@ -1,0 +1,203 @@
+// Format conversion between the reference's packed bytes
+// (pkg/src/qeft/packing.py:24-72: row-major, LSB-first; 4-bit even column in the
+// low nibble, 3-bit one bitstream per row padded to a byte) and the B200 tile
+// layout documented in qeft_common.cuh; plus the group-parameter / weak-column
+// packers, the input-column gather and a dequantize-to-dense debug kernel.
+#include "qeft_common.cuh"
+#include "qeft_internal.h"
+
+using namespace qeft;
+
+namespace {
+
+__device__ __forceinline__ int ref_code(const uint8_t* ref, int rbytes, int bits, int r, int j) {
+  const uint8_t* row = ref + (int64_t)r * rbytes;
+  if (bits == 4) {
+    const uint8_t b = row[j >> 1];
+    return (j & 1) ? (b >> 4) : (b & 15);
+  }
+  const int pos = 3 * j;  // LSB-first bitstream
+  uint32_t w = row[pos >> 3];
+  if ((pos >> 3) + 1 < rbytes) w |= (uint32_t)row[(pos >> 3) + 1] << 8;
+  return (w >> (pos & 7)) & 7;
+}
+
+__device__ __forceinline__ int tile_code(const uint32_t* qw, int bits, int m_pad, int r, int j) {
+  const CodeLoc L = locate_code(bits, m_pad, r, j);
+  if (bits == 4) return (qw[L.lo_word] >> L.lo_shift) & 15;
+  const int lo = (qw[L.lo_word] >> L.lo_shift) & 3;
+  const int hi = (qw[L.hi_word] >> L.hi_shift) & 1;
+  return lo | (hi << 2);
+}
+
+// one thread per code; the destination is zeroed beforehand
+__global__ void ref_to_tiles_kernel(const uint8_t* __restrict__ ref, int oc, int m, int bits,
+                                    int m_pad, uint32_t* __restrict__ qw) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)oc * m) return;
+  const int r = (int)(idx / m), j = (int)(idx % m);
+  const int rbytes = bits == 4 ? (m + 1) / 2 : (3 * m + 7) / 8;
+  const int c = ref_code(ref, rbytes, bits, r, j);
+  if (!c) return;
+  const CodeLoc L = locate_code(bits, m_pad, r, j);
+  if (bits == 4) {
+    atomicOr(qw + L.lo_word, (uint32_t)c << L.lo_shift);
+  } else {
+    if (c & 3) atomicOr(qw + L.lo_word, (uint32_t)(c & 3) << L.lo_shift);
+    if (c & 4) atomicOr(qw + L.hi_word, 1u << L.hi_shift);
+  }
+}
+
+// one thread per reference output byte
+__global__ void tiles_to_ref_kernel(const uint32_t* __restrict__ qw, int oc, int m, int bits,
+                                    int m_pad, uint8_t* __restrict__ ref) {
+  const int rbytes = bits == 4 ? (m + 1) / 2 : (3 * m + 7) / 8;
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)oc * rbytes) return;
+  const int r = (int)(idx / rbytes), b = (int)(idx % rbytes);
+  uint32_t out = 0;
+  if (bits == 4) {
+    const int j = 2 * b;
+    out = tile_code(qw, 4, m_pad, r, j);
+    if (j + 1 < m) out |= tile_code(qw, 4, m_pad, r, j + 1) << 4;
+  } else {
+    for (int bit = 0; bit < 8; ++bit) {
+      const int pos = 8 * b + bit, j = pos / 3;
+      if (j >= m) break;
+      out |= ((tile_code(qw, 3, m_pad, r, j) >> (pos % 3)) & 1u) << bit;
+    }
+  }
+  ref[idx] = (uint8_t)out;
+}
+
+template <typename T>
+__global__ void pack_sz_kernel(const float* __restrict__ scales, const float* __restrict__ zeros,
+                               int oc, int oc_pad, int ng, T* __restrict__ sz) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)oc_pad * ng) return;
+  const int r = (int)(idx / ng), gi = (int)(idx % ng);
+  float s = 0.f, z = 0.f;
+  if (r < oc) { s = scales[(int64_t)r * ng + gi]; z = zeros[(int64_t)r * ng + gi]; }
+  const int64_t o = (((int64_t)(r >> 4) * ng + gi) * 16 + (r & 15)) * 2;
+  sz[o] = from_f32<T>(s);
+  sz[o + 1] = from_f32<T>(z);
+}
+
+template <typename T>
+__global__ void pack_weak_kernel(const float* __restrict__ weak, int oc, int k, int oc_pad,
+                                 int k_pad, T* __restrict__ w16) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)oc_pad * k_pad) return;
+  const int r = (int)(idx / k_pad), j = (int)(idx % k_pad);
+  w16[idx] = from_f32<T>((r < oc && j < k) ? weak[(int64_t)r * k + j] : 0.f);
+}
+
+// out[r][col] (original column order, fp32) = dequantized code * s + z, weak restored
+template <typename T>
+__global__ void dequant_full_kernel(qeft_linear_t L, float* __restrict__ out) {
+  const int kk = L.m_pad + L.k_pad;
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)L.oc * kk) return;
+  const int r = (int)(idx / kk), j = (int)(idx % kk);
+  const int col = L.colmap[j];
+  if (col < 0) return;
+  float v;
+  if (j < L.m_pad) {
+    const int c = tile_code((const uint32_t*)L.qweight, L.bits, L.m_pad, r, j);
+    const int gi = min(j / L.g, L.ng - 1);
+    const T* sz = (const T*)L.sz + (((int64_t)(r >> 4) * L.ng + gi) * 16 + (r & 15)) * 2;
+    v = (float)c * to_f32<T>(sz[0]) + to_f32<T>(sz[1]);
+  } else {
+    v = to_f32<T>(((const T*)L.weak16)[(int64_t)r * L.k_pad + (j - L.m_pad)]);
+  }
+  out[(int64_t)r * L.ic + col] = v;
+}
+
+// xb[t][j] = colmap[j] >= 0 ? x[t][colmap[j]] : 0   (B200 K order)
+template <typename T>
+__global__ void gather_cols_kernel(const T* __restrict__ x, int64_t ldx, const int* __restrict__ colmap,
+                                   int kk, int rows, T* __restrict__ xb) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)rows * kk) return;
+  const int t = (int)(idx / kk), j = (int)(idx % kk);
+  const int c = colmap[j];
+  xb[idx] = c >= 0 ? x[(int64_t)t * ldx + c] : from_f32<T>(0.f);
+}
+
+inline unsigned nblk(int64_t n, int b = 256) { return (unsigned)((n + b - 1) / b); }
+
+}  // namespace
+
+namespace qeft {
+
+int repack_ref_to_tiles(const uint8_t* ref, int oc, int m, int bits, void* qw, cudaStream_t st) {
+  const int m_pad = pad_to(m, 128), oc_pad = pad_to(oc, 16);
+  const size_t bytes = (size_t)(oc_pad / 16) * rowblock_bytes(bits, m_pad);
+  QEFT_CUDA(cudaMemsetAsync(qw, 0, bytes, st));
+  if ((int64_t)oc * m == 0) return 0;
+  ref_to_tiles_kernel<<<nblk((int64_t)oc * m), 256, 0, st>>>(ref, oc, m, bits, m_pad, (uint32_t*)qw);
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int repack_tiles_to_ref(const void* qw, int oc, int m, int bits, uint8_t* ref, cudaStream_t st) {
+  const int m_pad = pad_to(m, 128);
+  const int rbytes = bits == 4 ? (m + 1) / 2 : (3 * m + 7) / 8;
+  if ((int64_t)oc * rbytes == 0) return 0;
+  tiles_to_ref_kernel<<<nblk((int64_t)oc * rbytes), 256, 0, st>>>((const uint32_t*)qw, oc, m, bits,
+                                                                 m_pad, ref);
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int pack_sz(const float* s, const float* z, int oc, int ng, int dtype, void* out, cudaStream_t st) {
+  const int oc_pad = pad_to(oc, 16);
+  if ((int64_t)oc_pad * ng == 0) return 0;
+  if (dtype == QEFT_F16)
+    pack_sz_kernel<__half><<<nblk((int64_t)oc_pad * ng), 256, 0, st>>>(s, z, oc, oc_pad, ng, (__half*)out);
+  else
+    pack_sz_kernel<__nv_bfloat16><<<nblk((int64_t)oc_pad * ng), 256, 0, st>>>(s, z, oc, oc_pad, ng,
+                                                                             (__nv_bfloat16*)out);
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int pack_weak(const float* w, int oc, int k, int dtype, void* out, cudaStream_t st) {
+  const int oc_pad = pad_to(oc, 16), k_pad = pad_to(k, 64);
+  if ((int64_t)oc_pad * k_pad == 0) return 0;
+  if (dtype == QEFT_F16)
+    pack_weak_kernel<__half><<<nblk((int64_t)oc_pad * k_pad), 256, 0, st>>>(w, oc, k, oc_pad, k_pad,
+                                                                           (__half*)out);
+  else
+    pack_weak_kernel<__nv_bfloat16><<<nblk((int64_t)oc_pad * k_pad), 256, 0, st>>>(
+        w, oc, k, oc_pad, k_pad, (__nv_bfloat16*)out);
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int dequant_full(const qeft_linear_t* L, float* out, cudaStream_t st) {
+  const int64_t n = (int64_t)L->oc * (L->m_pad + L->k_pad);
+  if (!n) return 0;
+  if (L->act_dtype == QEFT_F16)
+    dequant_full_kernel<__half><<<nblk(n), 256, 0, st>>>(*L, out);
+  else
+    dequant_full_kernel<__nv_bfloat16><<<nblk(n), 256, 0, st>>>(*L, out);
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int gather_cols(const void* x, int64_t ldx, const int* colmap, int kk, int rows, int dtype, void* xb,
+                cudaStream_t st) {
+  const int64_t n = (int64_t)rows * kk;
+  if (!n) return 0;
+  if (dtype == QEFT_F16)
+    gather_cols_kernel<__half><<<nblk(n), 256, 0, st>>>((const __half*)x, ldx, colmap, kk, rows,
+                                                        (__half*)xb);
+  else
+    gather_cols_kernel<__nv_bfloat16><<<nblk(n), 256, 0, st>>>(
+        (const __nv_bfloat16*)x, ldx, colmap, kk, rows, (__nv_bfloat16*)xb);
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace qeft

@@ -1,0 +1,230 @@
+"""Device-resident QEFT layer in the B200 tile layout, and the torch-level
+calls into the CUDA library (GEMV / GEMM / dequant).
+
+HBM layout of one layer (all on one GPU; see csrc/qeft_common.cuh):
+  qweight  uint8   (oc_pad/16) row-blocks x K-tiles of 512 B (4-bit) / 768 B (3-bit)
+  sz       dtype   (scale, zero) pairs [oc_pad/16][ng][16][2]
+  weak16   dtype   [oc_pad][k_pad]  (the trainable block's kernel shadow)
+  colmap   int32   [m_pad + k_pad]  B200 K position -> input column (-1 padding)
+  weak32   fp32    [oc][k]          trainable master (a view into the DP bucket
+                                     when the layer belongs to a model)
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .errors import ShapeError
+
+_DT = {"f16": _lib.QEFT_F16, "bf16": _lib.QEFT_BF16}
+
+
+def _pad(x: int, a: int) -> int:
+    return (x + a - 1) // a * a
+
+
+def torch_dtype(dtype: str):
+    import torch
+    return {"f16": torch.float16, "bf16": torch.bfloat16}[dtype]
+
+
+class _Workspace:
+    """Zero-initialised scratch shared by consecutive calls on one device.
+    Kernels that use split-K counters leave them zeroed again."""
+
+    def __init__(self):
+        self.buf = {}
+
+    def get(self, nbytes: int, device):
+        import torch
+        key = (str(device), torch.cuda.current_stream(device).cuda_stream)
+        b = self.buf.get(key)
+        if b is None or b.numel() < nbytes:
+            b = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+            self.buf[key] = b
+        return b
+
+
+WORKSPACE = _Workspace()
+
+
+class DeviceLayer:
+    """A QuantizedLinear converted to the B200 layout on the current GPU."""
+
+    def __init__(self, *, oc, ic, k, bits, g, qweight, sz, weak16, colmap, dtype="f16",
+                 weak32=None, structured_fast=False, source_id=None):
+        import torch
+        self.oc, self.ic, self.k, self.bits, self.g = oc, ic, k, bits, g
+        self.m = ic - k
+        self.ng = max(1, -(-self.m // g)) if self.m > 0 else 0
+        self.m_pad, self.k_pad, self.oc_pad = _pad(self.m, 128), _pad(k, 64), _pad(oc, 16)
+        self.dtype = dtype
+        self.tdtype = torch_dtype(dtype)
+        self.qweight, self.sz, self.weak16, self.colmap = qweight, sz, weak16, colmap
+        self.weak32 = weak32
+        self.structured_fast = structured_fast
+        self.source_id = source_id
+        self._refresh_struct()
+
+    def _refresh_struct(self):
+        s = _lib.QeftLinearT()
+        s.oc, s.ic, s.k, s.bits, s.g = self.oc, self.ic, self.k, self.bits, self.g
+        s.m, s.ng, s.m_pad, s.k_pad, s.oc_pad = self.m, self.ng, self.m_pad, self.k_pad, self.oc_pad
+        s.act_dtype = _DT[self.dtype]
+        s.flags = _lib.QEFT_FLAG_STRUCTURED_FAST if self.structured_fast else 0
+        s.qweight = self.qweight.data_ptr()
+        s.sz = self.sz.data_ptr()
+        s.weak16 = self.weak16.data_ptr() if self.weak16 is not None and self.weak16.numel() else None
+        s.colmap = self.colmap.data_ptr()
+        self.cstruct = s
+        self.cptr = ctypes.pointer(s)
+
+    @property
+    def device(self):
+        return self.qweight.device
+
+    def stale(self, q) -> bool:
+        return self.source_id != _source_id(q)
+
+    # ------------------------------------------------------------------
+    @classmethod
+    def from_quantized(cls, q, dtype="f16", device="cuda"):
+        """Upload + repack a QuantizedLinear (reference record) on the GPU."""
+        import torch
+        from .packing import to_tiles
+        oc, ic, k, bits, g = q.oc, q.ic, q.k, q.bits, q.g
+        m = ic - k
+        m_pad, k_pad = _pad(m, 128), _pad(k, 64)
+        qpos = q.quant_positions() if hasattr(q, "quant_positions") else None
+        widx = np.asarray(q.weak_indices, np.int64)
+        p = np.arange(ic) if q.input_perm is None else np.asarray(q.input_perm, np.int64)
+        colmap = np.full(m_pad + k_pad, -1, np.int32)
+        colmap[:m] = p[qpos]
+        colmap[m_pad:m_pad + k] = p[widx]
+        fast = (q.input_perm is None and q.layout == "structured" and m % 8 == 0 and ic % 8 == 0)
+        qweight = to_tiles(q.packed, oc, m, bits, device=device)
+        sc = torch.from_numpy(np.ascontiguousarray(q.scales, np.float32)).to(device)
+        zr = torch.from_numpy(np.ascontiguousarray(q.zeros, np.float32)).to(device)
+        ng = sc.shape[1]
+        sz = torch.empty((_pad(oc, 16) * ng * 2,), dtype=torch_dtype(dtype), device=device)
+        L = _lib.lib()
+        st = _lib.stream_ptr()
+        _lib.check(L.qeft_pack_sz(_lib.ptr(sc), _lib.ptr(zr), oc, ng, _DT[dtype], _lib.ptr(sz), st),
+                   "pack_sz")
+        weak32 = torch.from_numpy(np.ascontiguousarray(q.weak, np.float32)).to(device)
+        weak16 = torch.empty((_pad(oc, 16), k_pad), dtype=torch_dtype(dtype), device=device)
+        if k:
+            _lib.check(L.qeft_pack_weak(_lib.ptr(weak32), oc, k, _DT[dtype], _lib.ptr(weak16), st),
+                       "pack_weak")
+        return cls(oc=oc, ic=ic, k=k, bits=bits, g=g, qweight=qweight, sz=sz, weak16=weak16,
+                   colmap=torch.from_numpy(colmap).to(device), dtype=dtype,
+                   weak32=weak32.reshape(oc, k), structured_fast=fast, source_id=_source_id(q))
+
+    # ------------------------------------------------------------------
+    def refresh_weak16(self):
+        """Re-pack weak16 from the fp32 master (after an optimizer step)."""
+        if self.k:
+            _lib.check(_lib.lib().qeft_pack_weak(_lib.ptr(self.weak32), self.oc, self.k,
+                                                 _DT[self.dtype], _lib.ptr(self.weak16),
+                                                 _lib.stream_ptr()), "pack_weak")
+
+    def dequant_full(self):
+        """fp32 [oc][ic] as the kernels see it (fp16/bf16 params, weak16)."""
+        import torch
+        out = torch.zeros((self.oc, self.ic), dtype=torch.float32, device=self.device)
+        _lib.check(_lib.lib().qeft_dequant_full(self.cptr, _lib.ptr(out), _lib.stream_ptr()),
+                   "dequant_full")
+        return out
+
+    def weight_bytes(self) -> int:
+        """Algorithmic HBM bytes one GEMV must read (unpadded):
+        codes + fp16 (scale, zero) + fp16 weak block."""
+        from .packing import row_bytes
+        return self.oc * row_bytes(self.m, self.bits) + 4 * self.oc * self.ng + 2 * self.oc * self.k
+
+    # ------------------------------------------------------------------
+    def gemv(self, x, out=None, out_f32=False):
+        """y[n] = W_hat x[n] for x of shape (n, ic), n <= 16 (decode path)."""
+        import torch
+        _lib.require_cuda(x, "x")
+        if x.dim() != 2 or x.shape[1] != self.ic:
+            raise ShapeError(f"x shape {tuple(x.shape)} != (n, {self.ic})")
+        if x.dtype != self.tdtype:
+            raise ShapeError(f"x dtype {x.dtype} != layer dtype {self.tdtype}")
+        if x.stride(1) != 1:
+            x = x.contiguous()
+        n = x.shape[0]
+        if out is None:
+            out = torch.empty((n, self.oc), dtype=torch.float32 if out_f32 else self.tdtype,
+                              device=x.device)
+        L = _lib.lib()
+        wsb = int(L.qeft_gemv_workspace_bytes(self.cptr, n))
+        ws = WORKSPACE.get(wsb, x.device)
+        _lib.check(L.qeft_gemv(self.cptr, _lib.ptr(x), x.stride(0), _lib.ptr(out), out.stride(0),
+                               1 if out.dtype == torch.float32 else 0, n, _lib.ptr(ws), ws.numel(),
+                               _lib.stream_ptr()), "gemv")
+        return out
+
+    def gemm_fwd(self, x, out=None):
+        """y = x W_hat^T for x of shape (T, ic) (prefill / fine-tune forward)."""
+        import torch
+        _lib.require_cuda(x, "x")
+        if x.dim() != 2 or x.shape[1] != self.ic or x.dtype != self.tdtype:
+            raise ShapeError(f"x {tuple(x.shape)} {x.dtype} incompatible with layer")
+        if x.stride(1) != 1:
+            x = x.contiguous()
+        T = x.shape[0]
+        if out is None:
+            out = torch.empty((T, self.oc), dtype=self.tdtype, device=x.device)
+        L = _lib.lib()
+        ws = WORKSPACE.get(int(L.qeft_gemm_workspace_bytes(self.cptr, T)), x.device)
+        _lib.check(L.qeft_gemm_fwd(self.cptr, _lib.ptr(x), x.stride(0), _lib.ptr(out), out.stride(0),
+                                   T, _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "gemm_fwd")
+        return out
+
+    def gemm_dgrad(self, dy, out=None, accumulate=False):
+        """dx = dy W_hat for dy of shape (T, oc)."""
+        import torch
+        _lib.require_cuda(dy, "dy")
+        if dy.dim() != 2 or dy.shape[1] != self.oc or dy.dtype != self.tdtype:
+            raise ShapeError(f"dy {tuple(dy.shape)} {dy.dtype} incompatible with layer")
+        if dy.stride(1) != 1:
+            dy = dy.contiguous()
+        T = dy.shape[0]
+        if out is None:
+            out = torch.empty((T, self.ic), dtype=self.tdtype, device=dy.device)
+            accumulate = False
+        L = _lib.lib()
+        ws = WORKSPACE.get(int(L.qeft_gemm_workspace_bytes(self.cptr, T)), dy.device)
+        _lib.check(L.qeft_gemm_dgrad(self.cptr, _lib.ptr(dy), dy.stride(0), _lib.ptr(out),
+                                     out.stride(0), T, int(accumulate), _lib.ptr(ws), ws.numel(),
+                                     _lib.stream_ptr()), "gemm_dgrad")
+        return out
+
+    def gemm_wgrad(self, dy, x, out=None, accumulate=False):
+        """dW_weak[o][j] = sum_t dy[t][o] x[t][weak_j], fp32 (oc, k)."""
+        import torch
+        if dy.stride(1) != 1:
+            dy = dy.contiguous()
+        if x.stride(1) != 1:
+            x = x.contiguous()
+        T = dy.shape[0]
+        if out is None:
+            out = torch.empty((self.oc, self.k), dtype=torch.float32, device=dy.device)
+            accumulate = False
+        L = _lib.lib()
+        ws = WORKSPACE.get(int(L.qeft_gemm_workspace_bytes(self.cptr, T)), dy.device)
+        _lib.check(L.qeft_gemm_wgrad(self.cptr, _lib.ptr(dy), dy.stride(0), _lib.ptr(x), x.stride(0),
+                                     _lib.ptr(out), T, int(accumulate), _lib.ptr(ws), ws.numel(),
+                                     _lib.stream_ptr()), "gemm_wgrad")
+        return out
+
+
+def _source_id(q):
+    """Identity of the host record contents the device copy was built from."""
+    w = q.weak
+    return (id(q), q.packed.__hash__() if isinstance(q.packed, (bytes, bytearray)) else id(q.packed),
+            w.ctypes.data if isinstance(w, np.ndarray) else id(w))

@@ -1,0 +1,261 @@
+"""The QuantizedLinear record and `quantize_layer` (reference API).
+
+Mirrors pkg/src/qeft/quantizer.py: the record keeps the reference fields and
+byte format (so it interchanges with the reference's containers and tests);
+`quantize_layer` runs on the GPU:
+  * mode="rtn": min-max params + nearest codes in one CUDA kernel
+    (libqeft_b200 `qeft_quantize_rtn`), bit-exact with quantizer.py:115-120,
+    211-218;
+  * mode="optq": the alpha-grid parameter search (quantizer.py:144-179) and
+    the OPTQ column loop with inverse-Hessian error feedback
+    (quantizer.py:221-259), evaluated in fp64 on the GPU with torch linear
+    algebra (inv / cholesky). Codes match the reference except where the
+    BLAS/cuSOLVER rounding of H^-1 moves a value across a rounding boundary.
+Weak-column selection (irregular layouts) reuses calibration.select_local_topk
+and is bit-exact.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import ShapeError
+from .packing import pack_codes, unpack_codes
+
+LAYOUT_STRUCTURED = "structured"
+LAYOUT_IRREGULAR = "irregular"
+GRID_STEPS_DEFAULT = 100
+ALPHA_MIN_DEFAULT = 0.5
+OPTQ_DAMP_FRAC = 0.01
+
+
+def _n_groups(m: int, g: int) -> int:
+    return max(1, math.ceil(m / g)) if m > 0 else 0
+
+
+def group_slices(m: int, g: int):
+    """(start, stop) per group along the m quantized columns; last may be ragged
+    (quantizer.py:107-109)."""
+    return [(lo, min(lo + g, m)) for lo in range(0, m, g)]
+
+
+@dataclass
+class QuantizedLinear:
+    """Same fields and meaning as the reference record (quantizer.py:42-57)."""
+    oc: int
+    ic: int
+    k: int
+    bits: int
+    g: int
+    packed: bytes
+    scales: np.ndarray
+    zeros: np.ndarray
+    weak: np.ndarray
+    weak_indices: np.ndarray
+    layout: str
+    mode: str = "optq"
+    optq_fallback: bool = False
+    input_perm: np.ndarray | None = None
+
+    @property
+    def m(self) -> int:
+        return self.ic - self.k
+
+    @property
+    def n_groups(self) -> int:
+        return _n_groups(self.m, self.g)
+
+    def codes(self) -> np.ndarray:
+        return unpack_codes(self.packed, self.oc, self.m, self.bits)
+
+    def quant_positions(self) -> np.ndarray:
+        keep = np.ones(self.ic, dtype=bool)
+        keep[self.weak_indices] = False
+        return np.flatnonzero(keep)
+
+    def group_of(self, col: int) -> int:
+        return min(col // self.g, self.n_groups - 1) if self.m else 0
+
+    def dequant_dense(self) -> np.ndarray:
+        """Host view of the dequantized (oc, m) part, f32(code)*scale + zero
+        (quantizer.py:87-93); a format accessor, not the compute path."""
+        c = self.codes().astype(np.float32)
+        gidx = np.minimum(np.arange(self.m) // self.g, max(self.n_groups - 1, 0))
+        return c * self.scales[:, gidx] + self.zeros[:, gidx]
+
+    def dequant_full(self) -> np.ndarray:
+        out = np.empty((self.oc, self.ic), dtype=np.float32)
+        out[:, self.quant_positions()] = self.dequant_dense()
+        out[:, self.weak_indices] = self.weak
+        return out
+
+    # --- B200 device copy -------------------------------------------------
+    def device(self, dtype="f16"):
+        """The B200 tile-layout copy on the current CUDA device (cached)."""
+        from .layer import DeviceLayer
+        key = "_b200_" + dtype
+        dl = getattr(self, key, None)
+        if dl is None or dl.stale(self):
+            dl = DeviceLayer.from_quantized(self, dtype=dtype)
+            object.__setattr__(self, key, dl)
+        return dl
+
+
+# ---------------------------------------------------------------------------
+
+def _select_weak(ic, k, layout, lam, indices):
+    if layout == LAYOUT_STRUCTURED:
+        trailing = np.arange(ic - k, ic, dtype=np.int64)
+        if indices is not None and not np.array_equal(np.sort(np.asarray(indices)), trailing):
+            raise ShapeError("structured layout requires trailing weak columns")
+        return trailing
+    if layout == LAYOUT_IRREGULAR:
+        if indices is None:
+            if lam is None:
+                raise ShapeError("irregular layout needs indices or lambda")
+            from .calibration import select_local_topk
+            return select_local_topk(np.asarray(lam), k)
+        widx = np.sort(np.asarray(indices, dtype=np.int64))
+        if widx.size != k or (widx.size and (widx[0] < 0 or widx[-1] >= ic)):
+            raise ShapeError("weak index set invalid for layer")
+        if np.unique(widx).size != widx.size:
+            raise ShapeError("duplicate weak indices")
+        return widx
+    raise ShapeError(f"unknown layout {layout!r}")
+
+
+def _rtn_gpu(w_dense: np.ndarray, g: int, bits: int):
+    import torch
+    oc, m = w_dense.shape
+    ng = _n_groups(m, g)
+    wd = torch.from_numpy(np.ascontiguousarray(w_dense, np.float32)).cuda()
+    sc = torch.empty((oc, ng), dtype=torch.float32, device="cuda")
+    zr = torch.empty_like(sc)
+    codes = torch.empty((oc, m), dtype=torch.uint8, device="cuda")
+    _lib.check(_lib.lib().qeft_quantize_rtn(_lib.ptr(wd), oc, m, g, bits, _lib.ptr(sc), _lib.ptr(zr),
+                                            _lib.ptr(codes), _lib.stream_ptr()), "quantize_rtn")
+    return sc.cpu().numpy(), zr.cpu().numpy(), codes.cpu().numpy()
+
+
+def _grid_params_gpu(w_dense: np.ndarray, g: int, bits: int, steps: int, amin: float):
+    """alpha-grid search (quantizer.py:144-179) for every (row, group), fp64 on GPU."""
+    import torch
+    if steps < 1:
+        raise ShapeError("grid_steps must be >= 1")
+    w = torch.from_numpy(np.asarray(w_dense, np.float64)).cuda()
+    oc, m = w.shape
+    levels = 2 ** bits - 1
+    alphas = [1.0] if steps == 1 else list(amin + np.arange(steps) * (1.0 - amin) / (steps - 1))
+    al = torch.tensor(alphas, dtype=torch.float64, device="cuda")
+    is_one = al == 1.0
+    sc = torch.empty((oc, _n_groups(m, g)), dtype=torch.float64, device="cuda")
+    zr = torch.empty_like(sc)
+    for gi, (a, b) in enumerate(group_slices(m, g)):
+        seg = w[:, a:b]
+        wmin, wmax = seg.min(dim=1).values[:, None], seg.max(dim=1).values[:, None]
+        mid = 0.5 * (wmin + wmax)
+        lo = torch.where(is_one[None], wmin, mid - al[None] * (mid - wmin))
+        hi = torch.where(is_one[None], wmax, mid + al[None] * (wmax - mid))
+        s = (hi - lo) / levels                                      # (oc, A)
+        c = torch.clamp(torch.round((seg[:, None, :] - lo[..., None]) / s[..., None]), 0, levels)
+        err = ((seg[:, None, :] - (c * s[..., None] + lo[..., None])) ** 2).sum(-1)
+        pick = (err.shape[1] - 1) - torch.argmin(err.flip(1), dim=1)  # last min: larger alpha wins ties
+        s_best = s.gather(1, pick[:, None])[:, 0]
+        z_best = lo.gather(1, pick[:, None])[:, 0]
+        const = (wmax == wmin)[:, 0]
+        sc[:, gi] = torch.where(const, torch.ones_like(s_best), s_best)
+        zr[:, gi] = torch.where(const, wmin[:, 0], z_best)
+    return sc.float().cpu().numpy(), zr.float().cpu().numpy()
+
+
+def _optq_gpu(w_dense, h, sc, zr, g, bits):
+    """Greedy OPTQ rounding (quantizer.py:221-259) in fp64 on the GPU."""
+    import torch
+    w = torch.from_numpy(np.array(w_dense, np.float64)).cuda()
+    oc, m = w.shape
+    hd = torch.from_numpy(np.array(h, np.float64)).cuda()
+    hd.diagonal().add_(OPTQ_DAMP_FRAC * float(hd.diagonal().mean()))
+    try:
+        u = torch.linalg.cholesky(torch.linalg.inv(hd)).T.contiguous()
+        if not torch.isfinite(u).all():
+            raise RuntimeError("non-finite factor")
+    except RuntimeError:
+        return None
+    s64 = torch.from_numpy(sc.astype(np.float64)).cuda()
+    z64 = torch.from_numpy(zr.astype(np.float64)).cuda()
+    ng = s64.shape[1]
+    codes = torch.empty((oc, m), dtype=torch.uint8, device="cuda")
+    levels = 2 ** bits - 1
+    for i in range(m):
+        gi = min(i // g, ng - 1)
+        col = w[:, i]
+        q = torch.clamp(torch.round((col - z64[:, gi]) / s64[:, gi]), 0, levels)
+        codes[:, i] = q.to(torch.uint8)
+        e = (col - (q * s64[:, gi] + z64[:, gi])) / u[i, i]
+        if i + 1 < m:
+            w[:, i + 1:].sub_(torch.outer(e, u[i, i + 1:]))
+    return codes.cpu().numpy()
+
+
+def _nearest_codes_gpu(w_dense, sc, zr, g, bits):
+    """Independent nearest rounding on fixed params (quantizer.py:211-218), fp64 on GPU."""
+    import torch
+    oc, m = w_dense.shape
+    gidx = torch.clamp(torch.arange(m, device="cuda") // g, max=max(_n_groups(m, g) - 1, 0))
+    w = torch.from_numpy(np.asarray(w_dense, np.float64)).cuda()
+    s = torch.from_numpy(sc.astype(np.float64)).cuda()[:, gidx]
+    z = torch.from_numpy(zr.astype(np.float64)).cuda()[:, gidx]
+    c = torch.clamp(torch.round((w - z) / s), 0, 2 ** bits - 1)
+    return c.to(torch.uint8).cpu().numpy()
+
+
+def quantize_layer(w, *, k: int, bits: int, g: int, mode: str = "optq",
+                   layout: str = LAYOUT_STRUCTURED, lam=None, indices=None, x=None, h=None,
+                   grid_steps: int = GRID_STEPS_DEFAULT,
+                   alpha_min: float = ALPHA_MIN_DEFAULT) -> QuantizedLinear:
+    """Quantize one weight matrix into the mixed-precision layout
+    (reference signature and validation, quantizer.py:265-344)."""
+    w = np.asarray(w, dtype=np.float32)
+    oc, ic = w.shape
+    if k >= ic:
+        raise ShapeError(f"k={k} must be < IC={ic}")
+    if bits not in (3, 4):
+        raise ShapeError(f"bits must be 3 or 4, got {bits}")
+    if mode not in ("optq", "rtn"):
+        raise ShapeError(f"unknown mode {mode!r}")
+    widx = _select_weak(ic, k, layout, lam, indices)
+    keep = np.ones(ic, dtype=bool)
+    keep[widx] = False
+    qpos = np.flatnonzero(keep)
+    w_dense = np.ascontiguousarray(w[:, qpos])
+    m = w_dense.shape[1]
+    g_eff = min(g, m) if m else g
+    fallback = False
+    if mode == "rtn":
+        scales, zeros, codes = _rtn_gpu(w_dense, g_eff, bits)
+    else:
+        scales, zeros = _grid_params_gpu(w_dense, g_eff, bits, grid_steps, alpha_min)
+        if m > 0:
+            if h is None:
+                if x is None:
+                    raise ShapeError("optq mode needs calibration x or h")
+                xs = np.asarray(x, dtype=np.float64)
+                if xs.shape[0] != ic:
+                    raise ShapeError(f"calibration rows {xs.shape[0]} != IC {ic}")
+                h = 2.0 * xs @ xs.T
+            hq = np.asarray(h, dtype=np.float64)[np.ix_(qpos, qpos)]
+            if hq.shape != (m, m):
+                raise ShapeError(f"Hessian {hq.shape} does not match {m} columns")
+            codes = _optq_gpu(w_dense, hq, scales, zeros, g_eff, bits)
+            if codes is None:
+                codes, fallback = _nearest_codes_gpu(w_dense, scales, zeros, g_eff, bits), True
+        else:
+            codes = np.zeros((oc, 0), np.uint8)
+    return QuantizedLinear(
+        oc=oc, ic=ic, k=k, bits=bits, g=g_eff, packed=pack_codes(codes, bits),
+        scales=scales, zeros=zeros, weak=np.ascontiguousarray(w[:, widx]),
+        weak_indices=widx, layout=layout, mode=mode, optq_fallback=fallback)

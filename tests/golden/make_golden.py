@@ -1,0 +1,218 @@
+"""Generate golden parity fixtures by running the REFERENCE package itself.
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+It imports `qeft` from /root/reference/pkg/src (read-only), runs the hot-path
+functions on small seeded inputs and writes `tests/golden/*.npz`. The GPU box
+has no /root/reference; tests there read only these committed fixtures.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF = os.environ.get("QEFT_REFERENCE_SRC", "/root/reference/pkg/src")
+sys.path.insert(0, REF)
+sys.dont_write_bytecode = True
+
+from qeft import calibration, kernels, packing, quantizer, reorder, tuning  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def _layer_dict(prefix, q, d):
+    d[prefix + "oc"] = q.oc
+    d[prefix + "ic"] = q.ic
+    d[prefix + "k"] = q.k
+    d[prefix + "bits"] = q.bits
+    d[prefix + "g"] = q.g
+    d[prefix + "packed"] = np.frombuffer(q.packed, np.uint8)
+    d[prefix + "scales"] = q.scales
+    d[prefix + "zeros"] = q.zeros
+    d[prefix + "weak"] = q.weak
+    d[prefix + "weak_indices"] = q.weak_indices
+    d[prefix + "layout"] = q.layout
+    d[prefix + "fallback"] = q.optq_fallback
+
+
+def gen_packing():
+    d = {}
+    cases = []
+    for t in range(40):
+        rng = np.random.default_rng(100 + t)
+        bits = int(rng.choice([3, 4]))
+        oc, m = int(rng.integers(1, 20)), int(rng.integers(1, 70))
+        codes = rng.integers(0, 1 << bits, size=(oc, m)).astype(np.uint8)
+        d[f"c{t}_codes"] = codes
+        d[f"c{t}_bits"] = bits
+        d[f"c{t}_packed"] = np.frombuffer(packing.pack_codes(codes, bits), np.uint8)
+        cases.append(t)
+    d["n"] = len(cases)
+    np.savez_compressed(os.path.join(OUT, "packing.npz"), **d)
+
+
+def _rand_structured(rng):
+    # same family as pkg/tests/test_kernels.py:17-26
+    oc = int(rng.integers(1, 48))
+    ic = int(rng.integers(2, 80))
+    k = int(rng.integers(0, min(8, ic)))
+    g = int(rng.integers(1, 40))
+    bits = int(rng.choice([3, 4]))
+    w = (rng.standard_normal((oc, ic)) * rng.uniform(0.1, 3.0)).astype(np.float32)
+    return w, dict(k=k, bits=bits, g=g)
+
+
+def gen_quantizer():
+    d = {}
+    n = 0
+    # structured RTN family (kernel test family), seeds 0..59
+    for t in range(60):
+        rng = np.random.default_rng(t)
+        w, kw = _rand_structured(rng)
+        q = quantizer.quantize_layer(w, mode="rtn", layout="structured", **kw)
+        x = rng.standard_normal(q.ic).astype(np.float32)
+        d[f"q{n}_w"] = w
+        d[f"q{n}_mode"] = "rtn"
+        _layer_dict(f"q{n}_", q, d)
+        d[f"q{n}_x"] = x
+        d[f"q{n}_y_struct"] = kernels.matvec_structured(q, x)
+        d[f"q{n}_y_ref"] = kernels.matvec_reference(q, x)
+        n += 1
+    # grid-search params + OPTQ rounding, structured and irregular
+    for t in range(12):
+        rng = np.random.default_rng(700 + t)
+        oc, ic = int(rng.integers(4, 24)), int(rng.integers(12, 48))
+        k = int(rng.integers(0, 6))
+        g = int(rng.choice([4, 8, 16]))
+        bits = int(rng.choice([3, 4]))
+        w = rng.standard_normal((oc, ic)).astype(np.float32)
+        x = rng.standard_normal((ic, 32)).astype(np.float32)
+        layout = "structured" if t % 2 == 0 else "irregular"
+        extra = {}
+        if layout == "irregular":
+            extra["lam"] = np.abs(rng.standard_normal(ic))
+        q = quantizer.quantize_layer(w, k=k, bits=bits, g=g, mode="optq",
+                                     layout=layout, x=x, **extra)
+        d[f"q{n}_w"] = w
+        d[f"q{n}_mode"] = "optq"
+        d[f"q{n}_xcal"] = x
+        if "lam" in extra:
+            d[f"q{n}_lam"] = extra["lam"]
+        _layer_dict(f"q{n}_", q, d)
+        xv = rng.standard_normal(ic).astype(np.float32)
+        d[f"q{n}_x"] = xv
+        d[f"q{n}_y_ref"] = kernels.matvec_reference(q, xv)
+        if layout == "irregular":
+            d[f"q{n}_y_irr"] = kernels.matvec_irregular(q, xv)
+        else:
+            d[f"q{n}_y_struct"] = kernels.matvec_structured(q, xv)
+        n += 1
+    # pure grid-search parameter cases (outlier group, grid_steps=1)
+    d["grid_outlier_params"] = np.array(
+        [quantizer.grid_search_group_params(np.array([0.0, 1.0, 2.0, 100.0]), 2).scale,
+         quantizer.grid_search_group_params(np.array([0.0, 1.0, 2.0, 100.0]), 2).zero])
+    rng = np.random.default_rng(42)
+    segs = rng.standard_normal((30, 37))
+    gp = [quantizer.grid_search_group_params(s, 4) for s in segs]
+    d["grid_segs"] = segs
+    d["grid_scale"] = np.array([p.scale for p in gp])
+    d["grid_zero"] = np.array([p.zero for p in gp])
+    d["n"] = n
+    np.savez_compressed(os.path.join(OUT, "quantizer.npz"), **d)
+
+
+def gen_training():
+    d = {}
+    for t in range(10):
+        rng = np.random.default_rng(500 + t)
+        oc, ic = int(rng.integers(4, 40)), int(rng.integers(8, 64))
+        k = int(rng.integers(1, min(8, ic - 1)))
+        g = int(rng.choice([8, 16, 32]))
+        bits = int(rng.choice([3, 4]))
+        w = rng.standard_normal((oc, ic)).astype(np.float32)
+        layout = "structured" if t % 3 else "irregular"
+        extra = {} if layout == "structured" else {"lam": np.abs(rng.standard_normal(ic))}
+        q = quantizer.quantize_layer(w, k=k, bits=bits, g=g, mode="rtn",
+                                     layout=layout, **extra)
+        if t % 4 == 3:  # online variant: runtime input permutation
+            q.input_perm = rng.permutation(ic).astype(np.int64)
+        tt = int(rng.integers(2, 12))
+        x = rng.standard_normal((ic, tt)).astype(np.float32)
+        dy = rng.standard_normal((oc, tt)).astype(np.float32)
+        y, st = tuning.qlinear_forward_train(q, x)
+        c = tuning.CostCounters()
+        dx, dw = tuning.qlinear_backward(st, dy, q, counters=c)
+        _layer_dict(f"t{t}_", q, d)
+        d[f"t{t}_input_perm"] = (q.input_perm if q.input_perm is not None
+                                 else np.zeros(0, np.int64))
+        d[f"t{t}_x"], d[f"t{t}_dy"] = x, dy
+        d[f"t{t}_y"], d[f"t{t}_xw"] = y, st.x_weak
+        d[f"t{t}_dx"], d[f"t{t}_dw"] = dx, dw
+        d[f"t{t}_counters"] = np.array([c.wgrad_fma, c.full_fma, c.saved_elems, c.full_elems])
+    d["n"] = 10
+    # Adam trajectories
+    for t in range(3):
+        rng = np.random.default_rng(60 + t)
+        w = rng.standard_normal((5, 3)).astype(np.float32)
+        st = tuning.AdamState.like(w)
+        gs = rng.standard_normal((6, 5, 3)).astype(np.float32)
+        d[f"adam{t}_w0"] = w.copy()
+        d[f"adam{t}_g"] = gs
+        for s in range(6):
+            tuning.adam_step(st, w, gs[s], lr=0.01 * (t + 1))
+        d[f"adam{t}_w"] = w
+        d[f"adam{t}_m"], d[f"adam{t}_v"] = st.m, st.v
+    np.savez_compressed(os.path.join(OUT, "training.npz"), **d)
+
+
+def gen_selection():
+    d = {}
+    for t in range(6):
+        rng = np.random.default_rng(300 + t)
+        dm, ff, nb, k = 24, 48, 2, int(rng.integers(1, 6))
+        lam = {}
+        for b in range(nb):
+            for nm in ("wq", "wk", "wv", "wo", "w_up", "w_gate"):
+                v = np.abs(rng.standard_normal(dm))
+                if t % 2:
+                    v[rng.integers(0, dm, 3)] = 5.0  # ties
+                lam[f"b{b}.{nm}"] = v
+            lam[f"b{b}.w_down"] = np.abs(rng.standard_normal(ff))
+        lam["head"] = np.abs(rng.standard_normal(dm))
+        hd = calibration.HessianDiag(lam=lam, sample_count=1)
+        gwc = calibration.select_global(hd, k, n_blocks=nb)
+        for nm, v in lam.items():
+            d[f"s{t}_lam_{nm}"] = v
+        d[f"s{t}_names"] = np.array(list(lam.keys()))
+        d[f"s{t}_k"] = k
+        d[f"s{t}_resid"] = gwc.resid_indices
+        d[f"s{t}_sglobal"] = gwc.s_global
+        for b in range(nb):
+            d[f"s{t}_ffn{b}"] = gwc.ffn_indices[b]
+            d[f"s{t}_wo{b}"] = gwc.wo_indices[b]
+        d[f"s{t}_perm"] = reorder.weak_to_tail(dm, gwc.resid_indices).perm
+        # streaming lambda accumulation
+        run = None
+        xs = [rng.standard_normal((7, 5)) for _ in range(3)]
+        for x in xs:
+            run = calibration.accumulate_hessian_diag(
+                calibration.ForwardTrace({"l": x}, 5), run)
+        d[f"s{t}_lx"] = np.stack(xs)
+        d[f"s{t}_lam_stream"] = run.lam["l"]
+    d["n"] = 6
+    np.savez_compressed(os.path.join(OUT, "selection.npz"), **d)
+
+
+if __name__ == "__main__":
+    gen_packing()
+    gen_quantizer()
+    gen_training()
+    gen_selection()
+    for f in sorted(os.listdir(OUT)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(OUT, f)))

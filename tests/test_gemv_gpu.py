@@ -1,0 +1,240 @@
+"""GPU parity: format conversion, RTN quantizer, decode GEMV vs the CPU oracle.
+
+Bars (BASELINE.json north_star): packing / codes / indices bit-exact;
+floating-point outputs within max-rel 1e-2 of the fp64 oracle, metric
+max|y-ref| / max(1, max|ref|) (pkg/tests/test_kernels.py:37).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import qeft_oracle as O
+from tests.conftest import golden_layer, load_golden, rel_err
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-2
+
+
+@pytest.fixture(scope="module")
+def B():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2410_08661_b200 as pkg
+    from paper_2410_08661_b200 import kernels, layer, packing, quantizer
+    return pkg, kernels, layer, packing, quantizer
+
+
+def _as_product(q, quantizer):
+    return quantizer.QuantizedLinear(
+        oc=q.oc, ic=q.ic, k=q.k, bits=q.bits, g=q.g, packed=q.packed, scales=q.scales,
+        zeros=q.zeros, weak=q.weak, weak_indices=q.weak_indices, layout=q.layout,
+        input_perm=q.input_perm)
+
+
+# ---------------------------------------------------------------- packing ----
+
+def test_tile_round_trip_golden(B):
+    _, _, _, packing, _ = B
+    z = load_golden("packing")
+    for t in range(int(z["n"])):
+        codes, bits = z[f"c{t}_codes"], int(z[f"c{t}_bits"])
+        packed = z[f"c{t}_packed"].tobytes()
+        oc, m = codes.shape
+        assert packing.pack_codes(codes, bits) == packed
+        assert np.array_equal(packing.unpack_codes(packed, oc, m, bits), codes)
+        tiles = packing.to_tiles(packed, oc, m, bits)
+        assert packing.from_tiles(tiles, oc, m, bits) == packed
+
+
+@pytest.mark.parametrize("oc,m,bits", [(4096, 3968, 4), (33, 1000, 3), (17, 129, 4), (1, 1, 3),
+                                       (300, 2047, 3), (64, 128, 4)])
+def test_tile_round_trip_shapes(B, oc, m, bits):
+    _, _, _, packing, _ = B
+    rng = np.random.default_rng(oc * 7 + m)
+    codes = rng.integers(0, 1 << bits, size=(oc, m)).astype(np.uint8)
+    packed = packing.pack_codes(codes, bits)
+    assert packed == O.pack_codes(codes, bits) if oc * m < 20000 else True
+    assert packing.from_tiles(packing.to_tiles(packed, oc, m, bits), oc, m, bits) == packed
+
+
+# ---------------------------------------------------------------- quantizer --
+
+def test_quantize_rtn_bit_exact(B):
+    _, _, _, _, quantizer = B
+    z = load_golden("quantizer")
+    for n in range(int(z["n"])):
+        p = f"q{n}_"
+        if str(z[p + "mode"]) != "rtn":
+            continue
+        ref = golden_layer(z, p)
+        q = quantizer.quantize_layer(z[p + "w"], k=ref.k, bits=ref.bits, g=int(z[p + "g"]),
+                                     mode="rtn", layout=ref.layout)
+        assert q.packed == ref.packed, n
+        assert np.array_equal(q.scales, ref.scales) and np.array_equal(q.zeros, ref.zeros), n
+        assert np.array_equal(q.weak_indices, ref.weak_indices)
+
+
+def test_quantize_rtn_cfg1_bit_exact(B):
+    _, _, _, _, quantizer = B
+    rng = np.random.default_rng(0)
+    w = (rng.standard_normal((512, 4096)) * 0.02).astype(np.float32)
+    q = quantizer.quantize_layer(w, k=128, bits=4, g=128, mode="rtn")
+    o = O.quantize_layer(w, k=128, bits=4, g=128, mode="rtn")
+    assert q.packed == o.packed and np.array_equal(q.scales, o.scales)
+
+
+def test_quantize_optq_matches_reference(B):
+    _, _, _, _, quantizer = B
+    z = load_golden("quantizer")
+    total = same = 0
+    for n in range(int(z["n"])):
+        p = f"q{n}_"
+        if str(z[p + "mode"]) != "optq":
+            continue
+        ref = golden_layer(z, p)
+        kw = dict(x=z[p + "xcal"])
+        if p + "lam" in z:
+            kw["lam"] = z[p + "lam"]
+        q = quantizer.quantize_layer(z[p + "w"], k=ref.k, bits=ref.bits, g=ref.g, mode="optq",
+                                     layout=ref.layout, **kw)
+        # grid-search params: exact up to fp64 summation order of tied errors
+        assert np.mean(q.scales == ref.scales) >= 0.99
+        assert np.array_equal(q.weak_indices, ref.weak_indices)
+        c1, c2 = q.codes(), ref.codes()
+        total += c1.size
+        same += int(np.sum(c1 == c2))
+    assert same / total >= 0.99
+
+
+# ---------------------------------------------------------------- GEMV -------
+
+def test_gemv_randomized_family(B):
+    """The reference's 1000-case randomized family (pkg/tests/test_kernels.py:17-39)."""
+    _, kernels, _, _, quantizer = B
+    worst = 0.0
+    for t in range(1000):
+        rng = np.random.default_rng(t)
+        oc, ic = int(rng.integers(1, 48)), int(rng.integers(2, 80))
+        k = int(rng.integers(0, min(8, ic)))
+        g = int(rng.integers(1, 40))
+        bits = int(rng.choice([3, 4]))
+        w = (rng.standard_normal((oc, ic)) * rng.uniform(0.1, 3.0)).astype(np.float32)
+        q = O.quantize_layer(w, k=k, bits=bits, g=g, mode="rtn")
+        x = rng.standard_normal(ic).astype(np.float32)
+        y = kernels.matvec_structured(_as_product(q, quantizer), x)
+        worst = max(worst, rel_err(y, O.matvec_reference(q, x)))
+    assert worst <= TOL, worst
+
+
+def test_gemv_golden_optq_layers(B):
+    _, kernels, _, _, quantizer = B
+    z = load_golden("quantizer")
+    for n in range(int(z["n"])):
+        p = f"q{n}_"
+        q = golden_layer(z, p)
+        y = kernels.matvec_dispatch(_as_product(q, quantizer), z[p + "x"])
+        assert rel_err(y, z[p + "y_ref"]) <= TOL, n
+
+
+@pytest.mark.parametrize("bits,g,k", [(4, 128, 128), (3, 128, 128), (4, 64, 16), (3, 128, 64),
+                                      (4, 32, 8)])
+def test_gemv_llama_shape(B, bits, g, k):
+    _, kernels, _, _, quantizer = B
+    rng = np.random.default_rng(bits * 100 + k)
+    oc, ic = 4096, 4096
+    w = (rng.standard_normal((oc, ic)) * 0.02).astype(np.float32)
+    q = quantizer.quantize_layer(w, k=k, bits=bits, g=g, mode="rtn")
+    o = O.OracleLayer(oc=q.oc, ic=q.ic, k=q.k, bits=q.bits, g=q.g, packed=q.packed,
+                      scales=q.scales, zeros=q.zeros, weak=q.weak, weak_indices=q.weak_indices,
+                      layout=q.layout)
+    x = rng.standard_normal(ic).astype(np.float32)
+    y = kernels.matvec_structured(q, x)
+    assert rel_err(y, O.matvec_reference(o, x)) <= TOL
+
+
+def test_gemv_batch_columns_and_determinism(B):
+    import torch
+    _, _, _, _, quantizer = B
+    rng = np.random.default_rng(3)
+    w = (rng.standard_normal((1000, 2176)) * 0.05).astype(np.float32)
+    q = quantizer.quantize_layer(w, k=128, bits=4, g=128, mode="rtn")
+    dl = q.device("f16")
+    dq = dl.dequant_full().double()
+    for n in (1, 2, 5, 8, 9, 16):
+        x = torch.randn(n, 2176, device="cuda").half()
+        y1 = dl.gemv(x, out_f32=True)
+        y2 = dl.gemv(x, out_f32=True)
+        assert torch.equal(y1, y2)                       # deterministic split-K combine
+        ref = (x.double() @ dq.T)
+        assert rel_err(y1.cpu().numpy(), ref.cpu().numpy()) <= 2e-3
+        for j in range(n):                               # columns independent
+            yj = dl.gemv(x[j:j + 1], out_f32=True)
+            assert torch.allclose(yj[0], y1[j], rtol=0, atol=1e-4 * float(y1.abs().max()))
+
+
+def test_gemv_bf16_and_3bit_general_groups(B):
+    import torch
+    _, _, _, _, quantizer = B
+    rng = np.random.default_rng(4)
+    for bits, g, dt in ((4, 128, "bf16"), (3, 128, "bf16"), (4, 40, "f16"), (3, 24, "bf16")):
+        w = (rng.standard_normal((200, 1100)) * 0.05).astype(np.float32)
+        q = quantizer.quantize_layer(w, k=12, bits=bits, g=g, mode="rtn")
+        dl = q.device(dt)
+        x = torch.randn(3, 1100, device="cuda").to(dl.tdtype)
+        y = dl.gemv(x, out_f32=True)
+        o = O.OracleLayer(oc=q.oc, ic=q.ic, k=q.k, bits=q.bits, g=q.g, packed=q.packed,
+                          scales=q.scales, zeros=q.zeros, weak=q.weak,
+                          weak_indices=q.weak_indices, layout=q.layout)
+        ref = x.double().cpu().numpy() @ o.dequant_full().astype(np.float64).T
+        assert rel_err(y.cpu().numpy(), ref) <= TOL, (bits, g, dt)
+
+
+def test_gemv_irregular_and_online(B):
+    _, kernels, _, _, quantizer = B
+    z = load_golden("training")
+    for t in range(int(z["n"])):
+        p = f"t{t}_"
+        q = golden_layer(z, p)
+        ip = z[p + "input_perm"]
+        q.input_perm = ip if ip.size else None
+        qp = _as_product(q, quantizer)
+        x = z[p + "x"][:, 0]
+        y = kernels.matvec_dispatch(qp, x)
+        assert rel_err(y, O.matvec_reference(q, x)) <= TOL, t
+        if q.input_perm is not None:
+            assert rel_err(y, O.matvec_online_reorder(q, x, q.input_perm)) <= TOL
+
+
+def test_zero_input_and_weak_unit_vector(B):
+    """pkg/tests/test_kernels.py:41-44 and 62-72 (weak column comes back exactly,
+    here in the layer's fp16 storage precision)."""
+    _, kernels, _, _, quantizer = B
+    rng = np.random.default_rng(3)
+    w = rng.standard_normal((6, 12)).astype(np.float32)
+    qi = quantizer.quantize_layer(w, k=3, bits=4, g=4, mode="rtn", layout="irregular",
+                                  indices=np.array([2, 7, 11]))
+    x = np.zeros(12, np.float32)
+    assert np.all(kernels.matvec_irregular(qi, x) == 0.0)
+    x[7] = 1.0
+    assert np.array_equal(kernels.matvec_irregular(qi, x), w[:, 7].astype(np.float16).astype(np.float32))
+
+
+def test_counters_match_reference_formula(B):
+    _, kernels, _, packing, quantizer = B
+    q = quantizer.quantize_layer(np.ones((8, 20), np.float32), k=4, bits=4, g=8, mode="rtn")
+    st = kernels.KernelStats()
+    kernels.matvec_structured(q, np.ones(20, np.float32), st)
+    m, ng, oc, k = 16, 2, 8, 4
+    assert st.bytes_read == oc * packing.row_bytes(m, 4) + 2 * 4 * oc * ng + 4 * oc * k
+    assert st.fma == oc * m + 2 * oc * ng + oc * k and st.calls == 1 and st.elapsed_ns > 0
+
+
+def test_shape_errors(B):
+    _, kernels, _, _, quantizer = B
+    from paper_2410_08661_b200.errors import ShapeError
+    q = quantizer.quantize_layer(np.ones((8, 20), np.float32), k=4, bits=4, g=8, mode="rtn")
+    with pytest.raises(ShapeError):
+        kernels.matvec_structured(q, np.ones(21, np.float32))
+    with pytest.raises(ShapeError):
+        kernels.matvec_irregular(q, np.ones(20, np.float32))
