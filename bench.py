@@ -133,7 +133,7 @@ def cpu_oracle_sample(seconds: float = 10.0, seed: int = 0):
                                     zeros=zr, weak=weak, weak_indices=np.arange(m, ic),
                                     layout="structured"))
     xs = {ic: rng.standard_normal(ic).astype(np.float32) for _, ic in BLOCK_SHAPES}
-    nbytes = [O.row_bytes(q.m, 4) * q.oc + 4 * q.oc * q.n_groups + 2 * q.oc * q.k
+    nbytes = [O.row_bytes(q.m, 4) * q.oc + 8 * q.oc * q.n_groups + 2 * q.oc * q.k
               + 2 * (q.ic + q.oc) for q in layers]
     O.matvec_structured(layers[0], xs[layers[0].ic])  # warm
     done_b, calls, t0 = 0, 0, time.perf_counter()
@@ -267,6 +267,7 @@ def run_b200(args):
     e2e = ws * bytes_step * args.steps / te / 1e9
 
     roof = kernel_roofline(torch, min(args.blocks, 32), peak, n) if rank == 0 else []
+    n_layers = len(layers)
     del stack, layers
     line = None
     if rank == 0:
@@ -286,7 +287,7 @@ def run_b200(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
             "data": "synthetic",
             "config": {"workload": WORKLOAD, "n_cols": n, "blocks": args.blocks,
-                       "gemv_per_step": len(layers), "bytes_per_step": bytes_step,
+                       "gemv_per_step": n_layers, "bytes_per_step": bytes_step,
                        "l2": "inputs larger than L2 (%.2f GB of weights per step)" % (bytes_step / 1e9),
                        "parallelism": f"replicas{ws}"},
             "frac_of_peak": value / ws / peak, "peak_gbs": peak, "peak_kind": peak_kind,
@@ -296,7 +297,7 @@ def run_b200(args):
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                          "per_shape": roof},
             "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "gpu_launches": len(layers) * args.steps,
+            "gpu_launches": n_layers * args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }

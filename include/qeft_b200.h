@@ -48,10 +48,10 @@ typedef struct qeft_linear {
   int32_t m_pad;   /* roundup(m, 128) */
   int32_t k_pad;   /* roundup(k, 64), 0 when k == 0 */
   int32_t oc_pad;  /* roundup(oc, 16) */
-  int32_t act_dtype; /* QEFT_F16 / QEFT_BF16: dtype of sz, weak16, activations */
+  int32_t act_dtype; /* QEFT_F16 / QEFT_BF16: dtype of weak16 and activations */
   int32_t flags;
   const void* qweight;   /* tile-layout codes, (oc_pad/16) * rowblock bytes */
-  const void* sz;        /* (scale, zero) pairs [oc_pad/16][ng][16][2] */
+  const void* sz;        /* fp32 (scale, zero) pairs [oc_pad/16][ng][16][2] */
   const void* weak16;    /* [oc_pad][k_pad] */
   const int32_t* colmap; /* [m_pad + k_pad]: B200 K position -> input column, -1 pad */
 } qeft_linear_t;
@@ -67,9 +67,9 @@ int qeft_repack_to_tiles(const uint8_t* ref_packed, int oc, int m, int bits, voi
 /* Tiles -> reference packed bytes, bit-exact inverse (unpack/pack round trip). */
 int qeft_repack_to_ref(const void* qweight, int oc, int m, int bits, uint8_t* ref_packed,
                        void* stream);
-/* fp32 scales/zeros [oc][ng] (quantizer.py:50-51) -> sz pairs in act_dtype. */
-int qeft_pack_sz(const float* scales, const float* zeros, int oc, int ng, int act_dtype, void* sz,
-                 void* stream);
+/* fp32 scales/zeros [oc][ng] (quantizer.py:50-51) -> fp32 (scale, zero) pairs in the
+ * row-block-major sz layout (the reference's storage precision, 8 B per group). */
+int qeft_pack_sz(const float* scales, const float* zeros, int oc, int ng, void* sz, void* stream);
 /* fp32 weak block [oc][k] (quantizer.py:52) -> weak16 [oc_pad][k_pad]. */
 int qeft_pack_weak(const float* weak, int oc, int k, int act_dtype, void* weak16, void* stream);
 /* QuantizedLinear.dequant_full (quantizer.py:95-100) of the device layer, fp32 [oc][ic]. */

@@ -42,7 +42,7 @@ SIGNATURES = {
     "qeft_qweight_bytes": (_SZ, [_I, _I, _I]),
     "qeft_repack_to_tiles": (_I, [_VP, _I, _I, _I, _VP, _VP]),
     "qeft_repack_to_ref": (_I, [_VP, _I, _I, _I, _VP, _VP]),
-    "qeft_pack_sz": (_I, [_VP, _VP, _I, _I, _I, _VP, _VP]),
+    "qeft_pack_sz": (_I, [_VP, _VP, _I, _I, _VP, _VP]),
     "qeft_pack_weak": (_I, [_VP, _I, _I, _I, _VP, _VP]),
     "qeft_dequant_full": (_I, [_LP, _VP, _VP]),
     "qeft_gather_cols": (_I, [_VP, _I64, _VP, _I, _I, _I, _VP, _VP]),

@@ -57,8 +57,8 @@ int qeft_repack_to_ref(const void* qw, int oc, int m, int bits, uint8_t* ref, vo
   return repack_tiles_to_ref(qw, oc, m, bits, ref, ST(s));
 }
 
-int qeft_pack_sz(const float* sc, const float* zr, int oc, int ng, int dt, void* out, void* s) {
-  return pack_sz(sc, zr, oc, ng, dt, out, ST(s));
+int qeft_pack_sz(const float* sc, const float* zr, int oc, int ng, void* out, void* s) {
+  return pack_sz(sc, zr, oc, ng, out, ST(s));
 }
 
 int qeft_pack_weak(const float* w, int oc, int k, int dt, void* out, void* s) {

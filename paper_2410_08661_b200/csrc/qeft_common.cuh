@@ -27,6 +27,7 @@
 //     (quant positions, then weak indices; -1 for padding).
 #pragma once
 
+#include <cuda_runtime.h>
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -57,12 +58,14 @@ template <> struct DTraits<__half> {
   static constexpr uint32_t kMagic = 0x64006400u;   // fp16 1024.0 in both halves
   static constexpr float kMagicF = 1024.f;
   static constexpr bool kHiTrick = true;            // 1024 + 16c is exact in fp16
+  static constexpr uint32_t kOne2 = 0x3C003C00u;
 };
 template <> struct DTraits<__nv_bfloat16> {
   using T2 = __nv_bfloat162;
   static constexpr uint32_t kMagic = 0x43004300u;   // bf16 128.0
   static constexpr float kMagicF = 128.f;
   static constexpr bool kHiTrick = false;
+  static constexpr uint32_t kOne2 = 0x3F803F80u;
 };
 
 // 4-bit u32 -> four (magic + code) fragments (a0a1, a2a3, a4a5, a6a7).
@@ -118,6 +121,7 @@ template <> QEFT_DEV float to_f32<__nv_bfloat16>(__nv_bfloat16 v) { return __bfl
 template <typename T> QEFT_DEV T from_f32(float v);
 template <> QEFT_DEV __half from_f32<__half>(float v) { return __float2half_rn(v); }
 template <> QEFT_DEV __nv_bfloat16 from_f32<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+template <> QEFT_DEV float from_f32<float>(float v) { return v; }
 
 template <typename T2> QEFT_DEV float2 t2_to_f2(T2 v);
 template <> QEFT_DEV float2 t2_to_f2<__half2>(__half2 v) { return __half22float2(v); }
@@ -152,6 +156,113 @@ QEFT_DEV uint2 ldg_stream64(const void* p) {
   asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];\n"
                : "=r"(r.x), "=r"(r.y) : "l"(p));
   return r;
+}
+
+// ---- programmatic dependent launch (griddepcontrol) ----
+QEFT_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+QEFT_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+// Launch with cudaLaunchAttributeProgrammaticStreamSerialization so the kernel
+// may begin while its stream predecessor drains (it calls pdl_wait() before
+// touching the predecessor's outputs). Captured into CUDA graphs as
+// programmatic edges.
+template <typename Kern, typename... Args>
+inline cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  static const bool no_pdl = getenv("QEFT_NO_PDL") != nullptr;
+  cfg.attrs = attr;
+  cfg.numAttrs = no_pdl ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+template <typename Kern, typename... Args>
+inline cudaError_t launch_pdl_cluster(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                      int cluster_x, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster_x;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  static const bool no_pdl = getenv("QEFT_NO_PDL") != nullptr;
+  cfg.attrs = attr;
+  cfg.numAttrs = no_pdl ? 1 : 2;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+// ---- mbarrier / bulk async copy (TMA 1-D) ----
+QEFT_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+QEFT_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+QEFT_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+QEFT_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+QEFT_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+QEFT_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+QEFT_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0)
+QEFT_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---- clusters / distributed shared memory ----
+QEFT_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+QEFT_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
+// read a float from CTA `rank`'s shared memory at the same offset as local_addr
+QEFT_DEV float ld_dsmem_f32(uint32_t local_addr, uint32_t rank) {
+  uint32_t remote;
+  float v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(local_addr), "r"(rank));
+  asm volatile("ld.shared::cluster.f32 %0, [%1];\n" : "=f"(v) : "r"(remote) : "memory");
+  return v;
+}
+
+// weak16 element (r, j): row-block tiles of 16 rows x 64 columns (2 KB, contiguous),
+// tile (r/16, j/64) at ((r/16) * (k_pad/64) + j/64) * 1024 elements, row-major inside.
+__host__ __device__ inline int64_t weak_off(int r, int j, int k_pad) {
+  return (((int64_t)(r >> 4) * (k_pad >> 6) + (j >> 6)) << 10) + ((r & 15) << 6) + (j & 63);
 }
 
 // ---- code addressing in the tile layout (used by repack/debug kernels) ----

@@ -33,7 +33,7 @@ inline int pad_to(int x, int a) { return (x + a - 1) / a * a; }
 
 int repack_ref_to_tiles(const uint8_t* ref, int oc, int m, int bits, void* qw, cudaStream_t st);
 int repack_tiles_to_ref(const void* qw, int oc, int m, int bits, uint8_t* ref, cudaStream_t st);
-int pack_sz(const float* s, const float* z, int oc, int ng, int dtype, void* out, cudaStream_t st);
+int pack_sz(const float* s, const float* z, int oc, int ng, void* out, cudaStream_t st);
 int pack_weak(const float* w, int oc, int k, int dtype, void* out, cudaStream_t st);
 int dequant_full(const qeft_linear_t* L, float* out, cudaStream_t st);
 int gather_cols(const void* x, int64_t ldx, const int* colmap, int kk, int rows, int dtype, void* xb,

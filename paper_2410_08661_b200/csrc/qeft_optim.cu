@@ -118,9 +118,9 @@ __global__ void shadow_kernel(const float* __restrict__ w32, const qeft_shadow_d
     const int r = (int)(i / L.k), j = (int)(i % L.k);
     const float v = w32[L.offset + i];
     if (L.act_dtype == QEFT_F16)
-      put<__half>(L.weak16, (int64_t)r * L.k_pad + j, v);
+      put<__half>(L.weak16, weak_off(r, j, L.k_pad), v);
     else
-      put<__nv_bfloat16>(L.weak16, (int64_t)r * L.k_pad + j, v);
+      put<__nv_bfloat16>(L.weak16, weak_off(r, j, L.k_pad), v);
   }
 }
 

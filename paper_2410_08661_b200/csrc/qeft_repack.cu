@@ -89,7 +89,7 @@ __global__ void pack_weak_kernel(const float* __restrict__ weak, int oc, int k, 
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= (int64_t)oc_pad * k_pad) return;
   const int r = (int)(idx / k_pad), j = (int)(idx % k_pad);
-  w16[idx] = from_f32<T>((r < oc && j < k) ? weak[(int64_t)r * k + j] : 0.f);
+  w16[weak_off(r, j, k_pad)] = from_f32<T>((r < oc && j < k) ? weak[(int64_t)r * k + j] : 0.f);
 }
 
 // out[r][col] (original column order, fp32) = dequantized code * s + z, weak restored
@@ -105,10 +105,10 @@ __global__ void dequant_full_kernel(qeft_linear_t L, float* __restrict__ out) {
   if (j < L.m_pad) {
     const int c = tile_code((const uint32_t*)L.qweight, L.bits, L.m_pad, r, j);
     const int gi = min(j / L.g, L.ng - 1);
-    const T* sz = (const T*)L.sz + (((int64_t)(r >> 4) * L.ng + gi) * 16 + (r & 15)) * 2;
-    v = (float)c * to_f32<T>(sz[0]) + to_f32<T>(sz[1]);
+    const float* sz = (const float*)L.sz + (((int64_t)(r >> 4) * L.ng + gi) * 16 + (r & 15)) * 2;
+    v = (float)c * sz[0] + sz[1];
   } else {
-    v = to_f32<T>(((const T*)L.weak16)[(int64_t)r * L.k_pad + (j - L.m_pad)]);
+    v = to_f32<T>(((const T*)L.weak16)[weak_off(r, j - L.m_pad, L.k_pad)]);
   }
   out[(int64_t)r * L.ic + col] = v;
 }
@@ -150,14 +150,10 @@ int repack_tiles_to_ref(const void* qw, int oc, int m, int bits, uint8_t* ref, c
   return 0;
 }
 
-int pack_sz(const float* s, const float* z, int oc, int ng, int dtype, void* out, cudaStream_t st) {
+int pack_sz(const float* s, const float* z, int oc, int ng, void* out, cudaStream_t st) {
   const int oc_pad = pad_to(oc, 16);
   if ((int64_t)oc_pad * ng == 0) return 0;
-  if (dtype == QEFT_F16)
-    pack_sz_kernel<__half><<<nblk((int64_t)oc_pad * ng), 256, 0, st>>>(s, z, oc, oc_pad, ng, (__half*)out);
-  else
-    pack_sz_kernel<__nv_bfloat16><<<nblk((int64_t)oc_pad * ng), 256, 0, st>>>(s, z, oc, oc_pad, ng,
-                                                                             (__nv_bfloat16*)out);
+  pack_sz_kernel<float><<<nblk((int64_t)oc_pad * ng), 256, 0, st>>>(s, z, oc, oc_pad, ng, (float*)out);
   QEFT_CUDA(cudaGetLastError());
   return 0;
 }

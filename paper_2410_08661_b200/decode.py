@@ -45,12 +45,16 @@ def random_layer(oc, ic, k=128, bits=4, g=128, dtype="f16", seed=0, device="cuda
     s = 1e-3 + 0.01 * torch.randn(oc_pad, ng, device=device, generator=gen).abs()
     z = 0.05 * torch.randn(oc_pad, ng, device=device, generator=gen)
     sz = torch.stack([s, z], -1).reshape(oc_pad // 16, 16, ng, 2).permute(0, 2, 1, 3).contiguous()
-    weak16 = (0.02 * torch.randn(oc_pad, k_pad, device=device, generator=gen)).to(td)
-    weak16[:, k:] = 0
+    # weak16 in row-block tiles [oc_pad/16][k_pad/64][16][64] (csrc/qeft_common.cuh weak_off)
+    weak16 = (0.02 * torch.randn(oc_pad // 16, k_pad // 64, 16, 64, device=device, generator=gen)).to(td)
+    if k_pad:
+        col = (torch.arange(k_pad // 64, device=device)[:, None] * 64 + torch.arange(64, device=device))
+        weak16.masked_fill_((col >= k)[None, :, None, :], 0)
+    weak16 = weak16.reshape(oc_pad, k_pad)
     colmap = torch.full((m_pad + k_pad,), -1, dtype=torch.int32, device=device)
     colmap[:m] = torch.arange(m, dtype=torch.int32, device=device)
     colmap[m_pad:m_pad + k] = torch.arange(m, ic, dtype=torch.int32, device=device)
-    return DeviceLayer(oc=oc, ic=ic, k=k, bits=bits, g=g, qweight=qweight, sz=sz.to(td).reshape(-1),
+    return DeviceLayer(oc=oc, ic=ic, k=k, bits=bits, g=g, qweight=qweight, sz=sz.reshape(-1),
                        weak16=weak16, colmap=colmap, dtype=dtype,
                        structured_fast=(m % 8 == 0 and ic % 8 == 0))
 

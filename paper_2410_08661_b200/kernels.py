@@ -54,7 +54,7 @@ def analytic_fmas(q) -> int:
 def b200_bytes(q, n_cols: int = 1) -> int:
     """Algorithmic HBM bytes of one B200 GEMV (fp16 params/weak, fp16 x and y)."""
     from .packing import row_bytes
-    return (q.oc * row_bytes(q.m, q.bits) + 4 * q.oc * q.n_groups + 2 * q.oc * q.k
+    return (q.oc * row_bytes(q.m, q.bits) + 8 * q.oc * q.n_groups + 2 * q.oc * q.k
             + 2 * n_cols * (q.ic + q.oc))
 
 

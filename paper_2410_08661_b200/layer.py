@@ -109,11 +109,10 @@ class DeviceLayer:
         sc = torch.from_numpy(np.ascontiguousarray(q.scales, np.float32)).to(device)
         zr = torch.from_numpy(np.ascontiguousarray(q.zeros, np.float32)).to(device)
         ng = sc.shape[1]
-        sz = torch.empty((_pad(oc, 16) * ng * 2,), dtype=torch_dtype(dtype), device=device)
+        sz = torch.empty((_pad(oc, 16) * ng * 2,), dtype=torch.float32, device=device)
         L = _lib.lib()
         st = _lib.stream_ptr()
-        _lib.check(L.qeft_pack_sz(_lib.ptr(sc), _lib.ptr(zr), oc, ng, _DT[dtype], _lib.ptr(sz), st),
-                   "pack_sz")
+        _lib.check(L.qeft_pack_sz(_lib.ptr(sc), _lib.ptr(zr), oc, ng, _lib.ptr(sz), st), "pack_sz")
         weak32 = torch.from_numpy(np.ascontiguousarray(q.weak, np.float32)).to(device)
         weak16 = torch.empty((_pad(oc, 16), k_pad), dtype=torch_dtype(dtype), device=device)
         if k:
@@ -140,10 +139,10 @@ class DeviceLayer:
         return out
 
     def weight_bytes(self) -> int:
-        """Algorithmic HBM bytes one GEMV must read (unpadded):
-        codes + fp16 (scale, zero) + fp16 weak block."""
+        """Algorithmic HBM bytes one GEMV must read (unpadded): codes + fp32
+        (scale, zero) (the reference's analytic_bytes, kernels.py:54-58) + fp16 weak."""
         from .packing import row_bytes
-        return self.oc * row_bytes(self.m, self.bits) + 4 * self.oc * self.ng + 2 * self.oc * self.k
+        return self.oc * row_bytes(self.m, self.bits) + 8 * self.oc * self.ng + 2 * self.oc * self.k
 
     # ------------------------------------------------------------------
     def gemv(self, x, out=None, out_f32=False):
@@ -163,7 +162,9 @@ class DeviceLayer:
         L = _lib.lib()
         wsb = int(L.qeft_gemv_workspace_bytes(self.cptr, n))
         ws = WORKSPACE.get(wsb, x.device)
-        _lib.check(L.qeft_gemv(self.cptr, _lib.ptr(x), x.stride(0), _lib.ptr(out), out.stride(0),
+        ldx = x.stride(0) if n > 1 else self.ic      # size-1 dims may carry any stride
+        ldy = out.stride(0) if n > 1 else self.oc
+        _lib.check(L.qeft_gemv(self.cptr, _lib.ptr(x), ldx, _lib.ptr(out), ldy,
                                1 if out.dtype == torch.float32 else 0, n, _lib.ptr(ws), ws.numel(),
                                _lib.stream_ptr()), "gemv")
         return out
