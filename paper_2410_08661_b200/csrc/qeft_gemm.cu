@@ -1,23 +1,718 @@
-// tcgen05 prefill / fine-tune GEMMs (placeholder until the tcgen05 kernel lands).
+// Prefill / fine-tune GEMMs of the QEFT layer on 5th-generation tensor cores.
+//
+// Replaces the reference's dense fp32 products over the re-materialized weight
+// (pkg/src/qeft/tuning.py:52-103):
+//   fwd    Y[t][o]  = sum_j W_hat[o][j] X[t][j]            (qlinear_forward_train)
+//   dgrad  dX[t][i] = sum_o W_hat[o][i] dY[t][o]           (qlinear_backward, dX)
+//   wgrad  dW[o][w] = sum_t dY[t][o] X[t][weak_w]          (qlinear_backward, dW_weak)
+// W_hat is never materialized in HBM: warp-specialized persistent kernels
+//   * dequantize the 3/4-bit tile layout straight into SWIZZLE_128B shared memory
+//     (K-major for fwd, MN-major for dgrad) with 4 producer warps,
+//   * stream activations with TMA (cp.async.bulk.tensor, OOB zero fill covers the
+//     quantized/weak split of the B200 K order),
+//   * issue tcgen05.mma (M=128, N=BN, K=16, fp32 accumulators in TMEM, double
+//     buffered) from one thread,
+//   * drain TMEM with tcgen05.ld in 4 epilogue warps, transposing through shared
+//     memory into the row-major [tokens][channels] outputs.
+// wgrad is a smaller TMA-only kernel (both operands MN-major) whose N is the
+// weak block width.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
 #include "qeft_common.cuh"
 #include "qeft_internal.h"
+#include "qeft_tc.cuh"
+
+using namespace qeft;
+
+namespace {
+
+enum { MODE_FWD = 0, MODE_DGRAD = 1 };
+
+constexpr int BM = 128;                 // MMA M (rows of W_hat or of W_hat^T)
+constexpr int BK = 64;                  // K per stage (one SWIZZLE_128B row of fp16)
+constexpr int kProdWarps = 4;           // dequant producers
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = (2 + kProdWarps + kEpiWarps) * 32;  // TMA, MMA, producers, epilogue
+constexpr int kStageA = BM * BK * 2;    // 16 KB
+constexpr int kEpiStride = 40;          // halves per staging row (32 + 8 pad)
+
+struct GemmArgs {
+  const uint8_t* qw;
+  const float2* sz;
+  const void* weak16;
+  const int* colmap;
+  int oc, m, m_pad, k, k_pad, g, ng;
+  int T;
+  int n_mblk, n_nblk, n_kblk, kq;  // kq: quantized k-blocks (fwd) / quantized m-tiles (dgrad)
+  void* out;
+  int64_t ldo;
+  int accumulate;
+  int gathered;   // fwd: B from one map over a gathered B200-order buffer
+  int fast_out;   // dgrad: output columns contiguous in 32-blocks (structured, m % 32 == 0)
+  int out_cols;   // fwd: oc; dgrad: ic
+};
+
+template <typename T>
+QEFT_DEV uint32_t pack2(float a, float b) {
+  typename DTraits<T>::T2 v;
+  v.x = from_f32<T>(a);
+  v.y = from_f32<T>(b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// Dequantize one lane's share of a 16-row x 64-column k-tile (rows g, g+8 of the
+// row-block; columns 16t..16t+15) into fp32-exact (code*s + z) rounded to T.
+// q4 holds the lane's 4-bit word (16 B) or, for 3-bit, w2 (8 B) + hb (4 B).
+// out[0..7] = row g, cols 16t..16t+15 (T2 pairs); out[8..15] = row g+8.
+template <int BITS, typename T>
+QEFT_DEV void dequant_lane(const uint32_t* words, uint32_t hb, float2 p0, float2 p1, uint32_t out[16]) {
+  // magic + code halves via the fp16 trick for 4-bit (rows g+8 scaled by 16), exact in fp32
+  const float s0 = p0.x, z0 = p0.y - 1024.f * p0.x;
+  const float s1 = (BITS == 4) ? p1.x * (1.f / 16.f) : p1.x;
+  const float z1 = p1.y - 1024.f * s1;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t f[4];
+    if constexpr (BITS == 4) {
+      decode4<__half>(words[j], f);
+    } else {
+#pragma unroll
+      for (int pp = 0; pp < 4; ++pp) f[pp] = decode3_pair<__half>(words[j >> 1], hb, 4 * (j & 1) + pp, j >> 1);
+    }
+    const float2 a0 = __half22float2(*reinterpret_cast<__half2*>(&f[0]));  // row g, cols c, c+1
+    const float2 a1 = __half22float2(*reinterpret_cast<__half2*>(&f[1]));  // row g+8, cols c, c+1
+    const float2 a2 = __half22float2(*reinterpret_cast<__half2*>(&f[2]));  // row g, cols c+2, c+3
+    const float2 a3 = __half22float2(*reinterpret_cast<__half2*>(&f[3]));  // row g+8, cols c+2, c+3
+    out[2 * j] = pack2<T>(fmaf(a0.x, s0, z0), fmaf(a0.y, s0, z0));
+    out[2 * j + 1] = pack2<T>(fmaf(a2.x, s0, z0), fmaf(a2.y, s0, z0));
+    out[8 + 2 * j] = pack2<T>(fmaf(a1.x, s1, z1), fmaf(a1.y, s1, z1));
+    out[8 + 2 * j + 1] = pack2<T>(fmaf(a3.x, s1, z1), fmaf(a3.y, s1, z1));
+  }
+}
+
+// general group sizes: per-element (scale, zero)
+template <int BITS, typename T>
+QEFT_DEV void dequant_lane_general(const uint32_t* words, uint32_t hb, const float2* szrow0,
+                                   const float2* szrow1, int col0, int g, int ng, uint32_t out[16]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t f[4];
+    if constexpr (BITS == 4) {
+      decode4<__half>(words[j], f);
+    } else {
+#pragma unroll
+      for (int pp = 0; pp < 4; ++pp) f[pp] = decode3_pair<__half>(words[j >> 1], hb, 4 * (j & 1) + pp, j >> 1);
+    }
+    float v[2][4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int fi0 = (e < 2) ? 0 : 2, fi1 = (e < 2) ? 1 : 3;
+      const float2 h0 = __half22float2(*reinterpret_cast<__half2*>(&f[fi0]));
+      const float2 h1 = __half22float2(*reinterpret_cast<__half2*>(&f[fi1]));
+      const float c0 = ((e & 1) ? h0.y : h0.x) - 1024.f;
+      const float c1 = (BITS == 4) ? (((e & 1) ? h1.y : h1.x) - 1024.f) * (1.f / 16.f)
+                                   : ((e & 1) ? h1.y : h1.x) - 1024.f;
+      const int gi = min((col0 + 4 * j + e) / g, ng - 1);
+      const float2 pa = szrow0[gi * 16], pb = szrow1[gi * 16];
+      v[0][e] = c0 * pa.x + pa.y;
+      v[1][e] = c1 * pb.x + pb.y;
+    }
+    out[2 * j] = pack2<T>(v[0][0], v[0][1]);
+    out[2 * j + 1] = pack2<T>(v[0][2], v[0][3]);
+    out[8 + 2 * j] = pack2<T>(v[1][0], v[1][1]);
+    out[8 + 2 * j + 1] = pack2<T>(v[1][2], v[1][3]);
+  }
+}
+
+template <int MODE, int BITS, typename T, int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ CUtensorMap map_b1,
+            const GemmArgs a) {
+  constexpr int kStageB = BN * BK * 2;
+  constexpr int kStages = (BN == 256) ? 4 : 6;
+  constexpr int kTmemCols = 2 * BN;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte aligned base for SWIZZLE_128B atoms
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * kStageA;
+  T* sE = reinterpret_cast<T*>(sB + kStages * kStageB);  // epilogue staging [4 warps][32][kEpiStride]
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = a.n_mblk * a.n_nblk;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1 + kProdWarps);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tempty_bar[i], kEpiWarps);
+    }
+    fence_mbar_init();
+    tc::prefetch_tmap(&map_b0);
+    tc::prefetch_tmap(&map_b1);
+  }
+  if (warp == 1) tc::tmem_alloc(&tmem_base, kTmemCols);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+
+  pdl_launch_dependents();
+  pdl_wait();  // activations come from the previous kernel
+
+  if (warp == 0) {
+    // ================= TMA producer: activation tiles =================
+    if (lane == 0) {
+      int it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int n_blk = tile / a.n_mblk;
+        const int tok0 = n_blk * BN;
+        for (int kb = 0; kb < a.n_kblk; ++kb, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&empty_bar[s], ((it / kStages) & 1) ^ 1);
+          mbar_expect_tx(&full_bar[s], kStageB);
+          if (MODE == MODE_FWD && !a.gathered && kb >= a.kq)
+            tc::tma_load_2d(sB + s * kStageB, &map_b1, (kb - a.kq) * BK, tok0, &full_bar[s]);
+          else
+            tc::tma_load_2d(sB + s * kStageB, &map_b0, kb * BK, tok0, &full_bar[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer (one thread) =================
+    const uint32_t idesc = tc::idesc_f16(std::is_same<T, __nv_bfloat16>::value, BM, BN,
+                                         MODE == MODE_DGRAD, false);
+    int it = 0, tcount = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
+      const int acc = tcount & 1;
+      mbar_wait(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1);
+      tc::fence_after();
+      const uint32_t d_tmem = tmem + acc * BN;
+      for (int kb = 0; kb < a.n_kblk; ++kb, ++it) {
+        const int s = it % kStages;
+        mbar_wait(&full_bar[s], (it / kStages) & 1);
+        tc::fence_after();
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(sA + s * kStageA), b0 = smem_u32(sB + s * kStageB);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = (MODE == MODE_FWD) ? tc::smem_desc_sw128(a0 + 32 * k, 16, 1024)
+                                                   : tc::smem_desc_sw128(a0 + 2048 * k, 8192, 1024);
+            const uint64_t bd = tc::smem_desc_sw128(b0 + 32 * k, 16, 1024);
+            tc::mma_f16(d_tmem, ad, bd, idesc, (kb | k) ? 1u : 0u);
+          }
+          tc::commit(&empty_bar[s]);
+          if (kb == a.n_kblk - 1) tc::commit(&tfull_bar[acc]);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp < 2 + kProdWarps) {
+    // ================= dequant producers: the A operand =================
+    // Each warp fills two 16-row x 64-column units of the A tile per k-block:
+    //   fwd:   unit h = row-block 8*m_blk + 2*pw + h, B200 columns 64*kb.. (K-major rows)
+    //   dgrad: unit h = row-block 4*kb + pw, B200 columns 64*(2*m_blk + h).. (MN-major)
+    // Global loads for k-block kb+2 are issued before k-block kb is processed.
+    const int pw = warp - 2;
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const bool fold16 = (a.g % 16) == 0;
+    struct Pre {
+      uint4 v[2][4];   // quant: v[h][0] = lane codes (3-bit: .x,.y = 2-bit words, .z = hi word); weak: 64 B
+      float2 p0[2], p1[2];
+    };
+    // unit geometry: row-block, 64-column tile index in the B200 order, weak tile (or -1)
+    auto unit = [&](int m_blk, int kb, int h, int& rb, int& jt, int& kw) {
+      if (MODE == MODE_FWD) {
+        rb = m_blk * 8 + 2 * pw + h;
+        jt = kb;
+        kw = kb >= a.kq ? kb - a.kq : -1;
+      } else {
+        rb = kb * 4 + pw;
+        jt = 2 * m_blk + h;
+        kw = m_blk >= a.kq ? (m_blk - a.kq) * 2 + h : -1;
+      }
+    };
+    auto load = [&](int m_blk, int kb, Pre& P) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int rb, jt, kw;
+        unit(m_blk, kb, h, rb, jt, kw);
+        if (rb * 16 >= a.oc || (kw >= 0 && kw * 64 >= a.k_pad)) continue;
+        if (kw < 0) {
+          if constexpr (BITS == 4) {
+            P.v[h][0] = ldg_stream(a.qw + ((int64_t)rb * (a.m_pad >> 6) + jt) * 512 + lane * 16);
+          } else {
+            const uint8_t* tb = a.qw + ((int64_t)rb * (a.m_pad >> 7) + (jt >> 1)) * 768;
+            const uint2 w2 = *reinterpret_cast<const uint2*>(tb + lane * 16 + 8 * (jt & 1));
+            P.v[h][0] = make_uint4(w2.x, w2.y, *reinterpret_cast<const uint32_t*>(tb + 512 + lane * 8 + 4 * (jt & 1)), 0u);
+          }
+          if (fold16) {
+            const float2* szr = a.sz + (int64_t)rb * a.ng * 16;
+            const int gi = min((jt * BK + 16 * t4) / a.g, a.ng - 1);
+            P.p0[h] = szr[gi * 16 + g8];
+            P.p1[h] = szr[gi * 16 + g8 + 8];
+          }
+        } else {
+          const T* wt = (const T*)a.weak16 + ((int64_t)rb * (a.k_pad >> 6) + kw) * 1024;
+          P.v[h][0] = *reinterpret_cast<const uint4*>(wt + g8 * 64 + 16 * t4);
+          P.v[h][1] = *reinterpret_cast<const uint4*>(wt + g8 * 64 + 16 * t4 + 8);
+          P.v[h][2] = *reinterpret_cast<const uint4*>(wt + (g8 + 8) * 64 + 16 * t4);
+          P.v[h][3] = *reinterpret_cast<const uint4*>(wt + (g8 + 8) * 64 + 16 * t4 + 8);
+        }
+      }
+    };
+    auto process = [&](int m_blk, int kb, const Pre& P, uint8_t* st) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int rb, jt, kw;
+        unit(m_blk, kb, h, rb, jt, kw);
+        uint32_t out[16];
+        if (rb * 16 >= a.oc || (kw >= 0 && kw * 64 >= a.k_pad)) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) out[e] = 0u;
+        } else if (kw < 0) {
+          const uint32_t words[4] = {P.v[h][0].x, P.v[h][0].y, P.v[h][0].z, P.v[h][0].w};
+          const uint32_t hb = (BITS == 3) ? P.v[h][0].z : 0u;
+          if (fold16) {
+            dequant_lane<BITS, T>(words, hb, P.p0[h], P.p1[h], out);
+          } else {
+            const float2* szr = a.sz + (int64_t)rb * a.ng * 16;
+            dequant_lane_general<BITS, T>(words, hb, szr + g8, szr + g8 + 8, jt * BK + 16 * t4, a.g, a.ng, out);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            out[4 * q] = P.v[h][q].x; out[4 * q + 1] = P.v[h][q].y;
+            out[4 * q + 2] = P.v[h][q].z; out[4 * q + 3] = P.v[h][q].w;
+          }
+        }
+        uint32_t o0, o1, o2, o3;  // byte offsets of (row g, chunk 2t), (g, 2t+1), (g+8, 2t), (g+8, 2t+1)
+        if (MODE == MODE_FWD) {
+          const int r0 = 16 * (2 * pw + h) + g8, r1 = r0 + 8;
+          o0 = tc::sw128(r0, 2 * t4); o1 = tc::sw128(r0, 2 * t4 + 1);
+          o2 = tc::sw128(r1, 2 * t4); o3 = tc::sw128(r1, 2 * t4 + 1);
+        } else {
+          // MN-major: (m, k) at (m/64)*8192 + (k/8)*1024 + sw128(k%8, (m%64)/8)
+          const int kr0 = 16 * pw + g8, kr1 = kr0 + 8;
+          const uint32_t base = h * 8192;
+          o0 = base + (kr0 >> 3) * 1024 + tc::sw128(kr0 & 7, 2 * t4);
+          o1 = base + (kr0 >> 3) * 1024 + tc::sw128(kr0 & 7, 2 * t4 + 1);
+          o2 = base + (kr1 >> 3) * 1024 + tc::sw128(kr1 & 7, 2 * t4);
+          o3 = base + (kr1 >> 3) * 1024 + tc::sw128(kr1 & 7, 2 * t4 + 1);
+        }
+        *reinterpret_cast<uint4*>(st + o0) = make_uint4(out[0], out[1], out[2], out[3]);
+        *reinterpret_cast<uint4*>(st + o1) = make_uint4(out[4], out[5], out[6], out[7]);
+        *reinterpret_cast<uint4*>(st + o2) = make_uint4(out[8], out[9], out[10], out[11]);
+        *reinterpret_cast<uint4*>(st + o3) = make_uint4(out[12], out[13], out[14], out[15]);
+      }
+    };
+    // flatten (tile, kb) into one stream so the prefetch crosses tile boundaries
+    const int per = a.n_kblk;
+    const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int total = my_tiles * per;
+    auto coords = [&](int idx, int& m_blk, int& kb) {
+      const int tile = blockIdx.x + (idx / per) * gridDim.x;
+      m_blk = tile % a.n_mblk;
+      kb = idx % per;
+    };
+    Pre P0, P1, P2;  // register ring, rotated by value (no dynamic indexing -> no local memory)
+    if (total > 0) {
+      int mb, kb;
+      coords(0, mb, kb);
+      load(mb, kb, P0);
+    }
+    if (total > 1) {
+      int mb, kb;
+      coords(1, mb, kb);
+      load(mb, kb, P1);
+    }
+    for (int it = 0; it < total; ++it) {
+      if (it + 2 < total) {
+        int mb, kb;
+        coords(it + 2, mb, kb);
+        load(mb, kb, P2);
+      }
+      int mb, kb;
+      coords(it, mb, kb);
+      const int s = it % kStages;
+      mbar_wait(&empty_bar[s], ((it / kStages) & 1) ^ 1);
+      process(mb, kb, P0, sA + s * kStageA);
+      P0 = P1;
+      P1 = P2;
+      fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_bar[s]);
+    }
+  } else {
+    // ================= epilogue: TMEM -> registers -> smem transpose -> global =================
+    const int ew = warp - (2 + kProdWarps);
+    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    T* stg = sE + ew * 32 * kEpiStride;
+    int tcount = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
+      const int m_blk = tile % a.n_mblk, n_blk = tile / a.n_mblk;
+      const int acc = tcount & 1;
+      mbar_wait(&tfull_bar[acc], (tcount >> 1) & 1);
+      tc::fence_after();
+      const int row_base = m_blk * BM + quad * 32;  // channel (fwd) / B200 column (dgrad) of lane 0
+#pragma unroll 1
+      for (int cb = 0; cb < BN / 32; ++cb) {
+        uint32_t r[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + acc * BN + cb * 32, r);
+        // thread = one row (channel), 32 token columns -> staging [token][row]
+#pragma unroll
+        for (int c = 0; c < 32; ++c) stg[c * kEpiStride + lane] = from_f32<T>(__uint_as_float(r[c]));
+        __syncwarp();
+        // thread = one token, 32 consecutive rows
+        const int tok = n_blk * BN + cb * 32 + lane;
+        if (tok < a.T) {
+          const T* src = stg + lane * kEpiStride;
+          if (MODE == MODE_FWD || a.fast_out) {
+            int col0 = row_base;
+            if (MODE == MODE_DGRAD) col0 = row_base < a.m_pad ? row_base : a.m + (row_base - a.m_pad);
+            const int lim = (MODE == MODE_FWD) ? a.oc : ((row_base < a.m_pad) ? a.m : a.m + a.k);
+            T* dst = (T*)a.out + (int64_t)tok * a.ldo + col0;
+            const bool vec = (col0 + 32 <= lim) && ((((uintptr_t)dst) & 15) == 0);
+            if (vec && !a.accumulate) {
+#pragma unroll
+              for (int v = 0; v < 4; ++v)
+                reinterpret_cast<uint4*>(dst)[v] = reinterpret_cast<const uint4*>(src)[v];
+            } else {
+              for (int e = 0; e < 32 && col0 + e < lim; ++e)
+                dst[e] = a.accumulate ? from_f32<T>(to_f32<T>(dst[e]) + to_f32<T>(src[e])) : src[e];
+            }
+          } else {
+            for (int e = 0; e < 32; ++e) {
+              const int j = row_base + e;
+              if (j >= a.m_pad + a.k_pad) break;
+              const int col = a.colmap[j];
+              if (col < 0) continue;
+              T* dst = (T*)a.out + (int64_t)tok * a.ldo + col;
+              *dst = a.accumulate ? from_f32<T>(to_f32<T>(*dst) + to_f32<T>(src[e])) : src[e];
+            }
+          }
+        }
+        __syncwarp();
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+    }
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// wgrad: dW[o][w] (+)= sum_t dY[t][o] * Xw[t][w]; M = 128 channels, N = k_pad, K = tokens.
+// Both operands MN-major via TMA boxes of {64 (M or N), 64 (t)}.
+template <typename T, int NW>
+__global__ void __launch_bounds__(192, 1)
+wgrad_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_constant__ CUtensorMap map_xw,
+             float* __restrict__ dw, int oc, int k, int T_, int accumulate) {
+  constexpr int N = NW * 64;
+  constexpr int kSA = BM * 64 * 2;         // 16 KB: 2 boxes of 64 channels x 64 tokens
+  constexpr int kSB = N * 64 * 2;          // NW boxes of 64 weak columns x 64 tokens
+  constexpr int kStages = 4;
+  constexpr int kCols = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * kSA;
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], done_bar;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int o0 = blockIdx.x * BM;
+  const int nkb = (T_ + 63) / 64;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&done_bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(&tmem_base, kCols);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  pdl_launch_dependents();
+  pdl_wait();
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % kStages;
+        mbar_wait(&empty_bar[s], ((kb / kStages) & 1) ^ 1);
+        mbar_expect_tx(&full_bar[s], kSA + kSB);
+        tc::tma_load_2d(sA + s * kSA, &map_dy, o0, kb * 64, &full_bar[s]);
+        tc::tma_load_2d(sA + s * kSA + 8192, &map_dy, o0 + 64, kb * 64, &full_bar[s]);
+#pragma unroll
+        for (int b = 0; b < NW; ++b) tc::tma_load_2d(sB + s * kSB + b * 8192, &map_xw, b * 64, kb * 64, &full_bar[s]);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = tc::idesc_f16(std::is_same<T, __nv_bfloat16>::value, BM, N, true, true);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kStages;
+      mbar_wait(&full_bar[s], (kb / kStages) & 1);
+      tc::fence_after();
+      if (lane == 0) {
+        const uint32_t a0 = smem_u32(sA + s * kSA), b0 = smem_u32(sB + s * kSB);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          tc::mma_f16(tmem, tc::smem_desc_sw128(a0 + 2048 * kk, 8192, 1024),
+                      tc::smem_desc_sw128(b0 + 2048 * kk, 8192, 1024), idesc, (kb | kk) ? 1u : 0u);
+        tc::commit(&empty_bar[s]);
+        if (kb == nkb - 1) tc::commit(&done_bar);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int quad = warp & 3;
+    mbar_wait(&done_bar, 0);
+    tc::fence_after();
+    const int o = o0 + quad * 32 + lane;
+#pragma unroll 1
+    for (int cb = 0; cb < N / 32; ++cb) {
+      uint32_t r[32];
+      tc::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + cb * 32, r);
+      if (o < oc) {
+        float* dst = dw + (int64_t)o * k + cb * 32;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          if (cb * 32 + c < k) {
+            const float v = __uint_as_float(r[c]);
+            dst[c] = accumulate ? dst[c] + v : v;
+          }
+        }
+      }
+    }
+    tc::fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, kCols);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+// 2-D row-major [rows][ld] tensor, box {64 inner, box_rows}, SWIZZLE_128B, OOB -> 0
+int make_map(CUtensorMap* m, const void* base, int dtype, int64_t inner, int64_t rows, int64_t ld_elems,
+             int box_rows) {
+  auto fn = encode_fn();
+  QEFT_CHECK(fn != nullptr, QEFT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  QEFT_CHECK(((uintptr_t)base & 15) == 0 && (ld_elems * 2) % 16 == 0, QEFT_ERR_LAYOUT,
+             "TMA needs 16-byte aligned base and row stride");
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld_elems * 2)};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, dtype == QEFT_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  QEFT_CHECK(r == CUDA_SUCCESS, QEFT_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return 0;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int MODE, int BITS, typename T, int BN>
+int launch_gemm(const CUtensorMap& m0, const CUtensorMap& m1, const GemmArgs& a, cudaStream_t st) {
+  constexpr int kStageB = BN * BK * 2;
+  constexpr int kStages = (BN == 256) ? 4 : 6;
+  const size_t smem = 1024 + (size_t)kStages * (kStageA + kStageB) + (size_t)kEpiWarps * 32 * kEpiStride * 2;
+  auto kern = gemm_kernel<MODE, BITS, T, BN>;
+  static bool attr = false;
+  if (!attr) {
+    QEFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const int tiles = a.n_mblk * a.n_nblk;
+  const int grid = std::min(tiles, num_sms());
+  QEFT_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, m0, m1, a));
+  return 0;
+}
+
+template <int MODE, typename T>
+int dispatch_gemm(int bits, int T_, const CUtensorMap& m0, const CUtensorMap& m1, GemmArgs& a,
+                  cudaStream_t st) {
+  const bool big = T_ > 128;
+  const int BN = big ? 256 : 128;
+  a.n_nblk = (T_ + BN - 1) / BN;
+  if (bits == 4)
+    return big ? launch_gemm<MODE, 4, T, 256>(m0, m1, a, st) : launch_gemm<MODE, 4, T, 128>(m0, m1, a, st);
+  return big ? launch_gemm<MODE, 3, T, 256>(m0, m1, a, st) : launch_gemm<MODE, 3, T, 128>(m0, m1, a, st);
+}
+
+GemmArgs base_args(const qeft_linear_t* L, int T_) {
+  GemmArgs a{};
+  a.qw = (const uint8_t*)L->qweight;
+  a.sz = (const float2*)L->sz;
+  a.weak16 = L->weak16;
+  a.colmap = L->colmap;
+  a.oc = L->oc; a.m = L->m; a.m_pad = L->m_pad; a.k = L->k; a.k_pad = L->k_pad;
+  a.g = L->g; a.ng = L->ng;
+  a.T = T_;
+  return a;
+}
+
+}  // namespace
 
 namespace qeft {
 
-size_t gemm_workspace_bytes(const qeft_linear_t* L, int T) { (void)L; (void)T; return 0; }
+size_t gemm_workspace_bytes(const qeft_linear_t* L, int T_) {
+  // gathered activations in B200 K order (fwd, non-structured layouts), weak columns
+  // (wgrad), or a 16-byte-pitched copy of dY (dgrad/wgrad when oc % 8 != 0)
+  const size_t kk = (size_t)std::max(L->m_pad + L->k_pad, pad_to(L->oc, 8) + L->k_pad);
+  return (size_t)T_ * kk * 2 + 1024;
+}
 
-int gemm_fwd(const qeft_linear_t*, const void*, int64_t, void*, int64_t, int, void*, size_t, cudaStream_t) {
-  set_error("gemm_fwd: not built");
-  return QEFT_ERR_LAYOUT;
+// dY with a row pitch TMA cannot address -> copy into ws with pitch roundup(oc, 8)
+static int pitch_dy(const qeft_linear_t* L, const void*& dy, int64_t& lddy, int T_, void* ws,
+                    size_t ws_bytes, cudaStream_t st) {
+  if (lddy % 8 == 0 && ((uintptr_t)dy & 15) == 0) return 0;
+  const int ld = pad_to(L->oc, 8);
+  QEFT_CHECK(ws_bytes >= (size_t)T_ * ld * 2, QEFT_ERR_SHAPE, "workspace too small for dY copy");
+  QEFT_CUDA(cudaMemset2DAsync(ws, (size_t)ld * 2, 0, (size_t)ld * 2, T_, st));
+  QEFT_CUDA(cudaMemcpy2DAsync(ws, (size_t)ld * 2, dy, (size_t)lddy * 2, (size_t)L->oc * 2, T_,
+                              cudaMemcpyDeviceToDevice, st));
+  dy = ws;
+  lddy = ld;
+  return 0;
 }
-int gemm_dgrad(const qeft_linear_t*, const void*, int64_t, void*, int64_t, int, int, void*, size_t,
-               cudaStream_t) {
-  set_error("gemm_dgrad: not built");
-  return QEFT_ERR_LAYOUT;
+
+int gemm_fwd(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ldy, int T_, void* ws,
+             size_t ws_bytes, cudaStream_t st) {
+  QEFT_CHECK(T_ >= 1, QEFT_ERR_SHAPE, "gemm_fwd: T=%d", T_);
+  QEFT_CHECK(ldx >= L->ic && ldy >= L->oc, QEFT_ERR_SHAPE, "gemm_fwd: ld too small");
+  GemmArgs a = base_args(L, T_);
+  a.n_mblk = (L->oc_pad + BM - 1) / BM;
+  a.kq = L->m_pad / BK;
+  a.n_kblk = a.kq + L->k_pad / BK;
+  a.out = y;
+  a.ldo = ldy;
+  a.out_cols = L->oc;
+  CUtensorMap m0, m1;
+  const bool fast = (L->flags & QEFT_FLAG_STRUCTURED_FAST) && ldx % 8 == 0 && ((uintptr_t)x & 15) == 0;
+  const int box = T_ > 128 ? 256 : 128;
+  if (fast) {
+    if (int r = make_map(&m0, x, L->act_dtype, L->m, T_, ldx, box)) return r;
+    const void* xw = (const char*)x + (size_t)L->m * 2;
+    if (int r = make_map(&m1, xw, L->act_dtype, std::max(L->k, 1), T_, ldx, box)) return r;
+  } else {
+    const int kk = L->m_pad + L->k_pad;
+    QEFT_CHECK(ws_bytes >= (size_t)T_ * kk * 2, QEFT_ERR_SHAPE, "gemm_fwd: workspace too small");
+    if (int r = gather_cols(x, ldx, L->colmap, kk, T_, L->act_dtype, ws, st)) return r;
+    if (int r = make_map(&m0, ws, L->act_dtype, kk, T_, kk, box)) return r;
+    m1 = m0;
+    a.gathered = 1;
+  }
+  if (L->act_dtype == QEFT_F16) return dispatch_gemm<MODE_FWD, __half>(L->bits, T_, m0, m1, a, st);
+  return dispatch_gemm<MODE_FWD, __nv_bfloat16>(L->bits, T_, m0, m1, a, st);
 }
-int gemm_wgrad(const qeft_linear_t*, const void*, int64_t, const void*, int64_t, float*, int, int, void*,
-               size_t, cudaStream_t) {
-  set_error("gemm_wgrad: not built");
+
+int gemm_dgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, void* dx, int64_t lddx, int T_,
+               int accumulate, void* ws, size_t ws_bytes, cudaStream_t st) {
+  QEFT_CHECK(T_ >= 1, QEFT_ERR_SHAPE, "gemm_dgrad: T=%d", T_);
+  QEFT_CHECK(lddy >= L->oc && lddx >= L->ic, QEFT_ERR_SHAPE, "gemm_dgrad: ld too small");
+  if (int r = pitch_dy(L, dy, lddy, T_, ws, ws_bytes, st)) return r;
+  GemmArgs a = base_args(L, T_);
+  a.n_mblk = (L->m_pad + L->k_pad + BM - 1) / BM;
+  a.kq = L->m_pad / BM;
+  a.n_kblk = (L->oc_pad + BK - 1) / BK;
+  a.out = dx;
+  a.ldo = lddx;
+  a.accumulate = accumulate;
+  a.out_cols = L->ic;
+  a.fast_out = (L->flags & QEFT_FLAG_STRUCTURED_FAST) && (L->m % 32 == 0);
+  CUtensorMap m0;
+  const int box = T_ > 128 ? 256 : 128;
+  if (int r = make_map(&m0, dy, L->act_dtype, L->oc, T_, lddy, box)) return r;
+  if (L->act_dtype == QEFT_F16) return dispatch_gemm<MODE_DGRAD, __half>(L->bits, T_, m0, m0, a, st);
+  return dispatch_gemm<MODE_DGRAD, __nv_bfloat16>(L->bits, T_, m0, m0, a, st);
+}
+
+template <typename T, int NW>
+int launch_wgrad(const CUtensorMap& md, const CUtensorMap& mx, float* dw, int oc, int k, int T_, int acc,
+                 cudaStream_t st) {
+  constexpr int kStages = 4;
+  const size_t smem = 1024 + (size_t)kStages * (BM * 64 * 2 + NW * 64 * 64 * 2);
+  auto kern = wgrad_kernel<T, NW>;
+  static bool attr = false;
+  if (!attr) {
+    QEFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  QEFT_CUDA(launch_pdl(kern, dim3((oc + BM - 1) / BM), dim3(192), smem, st, md, mx, dw, oc, k, T_, acc));
+  return 0;
+}
+
+int gemm_wgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, const void* x, int64_t ldx, float* dw,
+               int T_, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st) {
+  QEFT_CHECK(T_ >= 1, QEFT_ERR_SHAPE, "gemm_wgrad: T=%d", T_);
+  if (L->k == 0) return 0;
+  QEFT_CHECK(L->k_pad <= 256, QEFT_ERR_LAYOUT, "gemm_wgrad: k_pad=%d > 256", L->k_pad);
+  CUtensorMap md, mx;
+  // workspace: [weak columns of x (T x k_pad)] [pitched dY copy]
+  const size_t xw_bytes = (size_t)T_ * L->k_pad * 2;
+  void* ws_dy = (char*)ws + ((xw_bytes + 255) & ~(size_t)255);
+  const size_t ws_dy_bytes = ws_bytes > ((xw_bytes + 255) & ~(size_t)255) ? ws_bytes - ((xw_bytes + 255) & ~(size_t)255) : 0;
+  if (int r = pitch_dy(L, dy, lddy, T_, ws_dy, ws_dy_bytes, st)) return r;
+  if (int r = make_map(&md, dy, L->act_dtype, L->oc, T_, lddy, 64)) return r;
+  const bool fast = (L->flags & QEFT_FLAG_STRUCTURED_FAST) && ldx % 8 == 0 && ((uintptr_t)x & 15) == 0;
+  if (fast) {
+    if (int r = make_map(&mx, (const char*)x + (size_t)L->m * 2, L->act_dtype, L->k, T_, ldx, 64)) return r;
+  } else {
+    QEFT_CHECK(ws_bytes >= xw_bytes, QEFT_ERR_SHAPE, "gemm_wgrad: workspace too small");
+    if (int r = gather_cols(x, ldx, L->colmap + L->m_pad, L->k_pad, T_, L->act_dtype, ws, st)) return r;
+    if (int r = make_map(&mx, ws, L->act_dtype, L->k_pad, T_, L->k_pad, 64)) return r;
+  }
+  const int nw = L->k_pad / 64;
+  const bool bf = L->act_dtype == QEFT_BF16;
+#define QEFT_WG(NW)                                                                              \
+  if (nw == NW)                                                                                  \
+    return bf ? launch_wgrad<__nv_bfloat16, NW>(md, mx, dw, L->oc, L->k, T_, accumulate, st)     \
+              : launch_wgrad<__half, NW>(md, mx, dw, L->oc, L->k, T_, accumulate, st);
+  QEFT_WG(1) QEFT_WG(2) QEFT_WG(3) QEFT_WG(4)
+#undef QEFT_WG
+  set_error("gemm_wgrad: unsupported k_pad");
   return QEFT_ERR_LAYOUT;
 }
 

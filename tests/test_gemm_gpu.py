@@ -1,0 +1,102 @@
+"""GPU parity of the tcgen05 GEMMs (fwd, dgrad, wgrad) against the CPU oracle
+(reference golden vectors, tuning.py:52-103) and an fp64 product over the
+device-dequantized weights. Tolerance: max-rel 1e-2 (BASELINE.json north_star),
+metric max|y-ref| / max(1, max|ref|)."""
+
+import numpy as np
+import pytest
+
+from oracle import qeft_oracle as O
+from tests.conftest import golden_layer, load_golden, rel_err
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-2
+
+
+@pytest.fixture(scope="module")
+def Q():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2410_08661_b200 import quantizer
+    return quantizer
+
+
+def _layer(quantizer, oc, ic, k, bits, g, layout="structured", seed=0, perm=False):
+    rng = np.random.default_rng(seed)
+    w = (rng.standard_normal((oc, ic)) * 0.05).astype(np.float32)
+    kw = {}
+    if layout == "irregular":
+        kw["lam"] = np.abs(rng.standard_normal(ic))
+    q = quantizer.quantize_layer(w, k=k, bits=bits, g=g, mode="rtn", layout=layout, **kw)
+    if perm:
+        q.input_perm = rng.permutation(ic).astype(np.int64)
+    return q
+
+
+CASES = [
+    # oc, ic, k, bits, g, dtype, T, layout, perm
+    (512, 1024, 128, 4, 128, "bf16", 256, "structured", False),
+    (512, 1024, 128, 4, 128, "f16", 100, "structured", False),
+    (4096, 4096, 128, 4, 128, "bf16", 512, "structured", False),
+    (300, 2176, 64, 4, 64, "f16", 300, "structured", False),
+    (200, 1100, 12, 3, 128, "bf16", 33, "structured", False),
+    (256, 768, 64, 3, 128, "bf16", 130, "structured", False),
+    (160, 512, 16, 4, 32, "bf16", 64, "irregular", False),
+    (128, 384, 32, 4, 64, "bf16", 200, "structured", True),
+    (96, 200, 8, 4, 40, "f16", 17, "structured", False),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_fwd_dgrad_wgrad_vs_fp64(Q, case):
+    import torch
+    oc, ic, k, bits, g, dt, T, layout, perm = case
+    q = _layer(Q, oc, ic, k, bits, g, layout, seed=oc + ic, perm=perm)
+    dl = q.device(dt)
+    # W_hat placed at the ORIGINAL input columns: online-reorder layers read x[input_perm]
+    # (tuning.py:64-65) and un-permute dX (tuning.py:93-96), which this absorbs
+    dq = dl.dequant_full().double()
+    x = torch.randn(T, ic, device="cuda").to(dl.tdtype)
+    dy = torch.randn(T, oc, device="cuda").to(dl.tdtype)
+    y = dl.gemm_fwd(x)
+    ref = x.double() @ dq.T
+    assert rel_err(y.float().cpu().numpy(), ref.cpu().numpy()) <= TOL
+    dx = dl.gemm_dgrad(dy)
+    dref = dy.double() @ dq
+    assert rel_err(dx.float().cpu().numpy(), dref.cpu().numpy()) <= TOL
+    # wgrad on the weak columns x[:, P[weak_indices]]
+    p = q.input_perm if perm else np.arange(ic)
+    widx = torch.from_numpy(p[q.weak_indices]).cuda()
+    dw = dl.gemm_wgrad(dy, x)
+    wref = dy.double().T @ x[:, widx].double()
+    assert rel_err(dw.cpu().numpy(), wref.cpu().numpy()) <= TOL
+    # accumulate paths
+    dw2 = dl.gemm_wgrad(dy, x, out=dw.clone(), accumulate=True)
+    assert rel_err(dw2.cpu().numpy(), 2 * wref.cpu().numpy()) <= TOL
+    dx2 = dl.gemm_dgrad(dy, out=dx.clone(), accumulate=True)
+    assert rel_err(dx2.float().cpu().numpy(), 2 * dref.cpu().numpy()) <= TOL
+
+
+def test_train_golden_vs_reference(Q):
+    """Reference qlinear_forward_train / qlinear_backward golden vectors
+    (tests/golden/training.npz, made by pkg/src/qeft/tuning.py)."""
+    import torch
+    z = load_golden("training")
+    for t in range(int(z["n"])):
+        p = f"t{t}_"
+        o = golden_layer(z, p)
+        ip = z[p + "input_perm"]
+        q = Q.QuantizedLinear(oc=o.oc, ic=o.ic, k=o.k, bits=o.bits, g=o.g, packed=o.packed,
+                              scales=o.scales, zeros=o.zeros, weak=o.weak,
+                              weak_indices=o.weak_indices, layout=o.layout,
+                              input_perm=ip if ip.size else None)
+        dl = q.device("f16")
+        x = torch.from_numpy(z[p + "x"].T.copy()).cuda().half()     # (T, ic)
+        dy = torch.from_numpy(z[p + "dy"].T.copy()).cuda().half()   # (T, oc)
+        y = dl.gemm_fwd(x).float().cpu().numpy().T
+        assert rel_err(y, z[p + "y"]) <= TOL, t
+        dx = dl.gemm_dgrad(dy).float().cpu().numpy().T
+        assert rel_err(dx, z[p + "dx"]) <= TOL, t
+        dw = dl.gemm_wgrad(dy, x).cpu().numpy()
+        assert rel_err(dw, z[p + "dw"]) <= TOL, t
