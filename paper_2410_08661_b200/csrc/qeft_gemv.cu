@@ -3,33 +3,34 @@
 // Replaces the reference's matvec paths (pkg/src/qeft/kernels.py:66-157,
 // `_grouped_accumulate`): y = sum_g s_g * (c_g . x_g) + z_g * sum(x_g) + W_weak . x_weak.
 //
-// HBM-bound design for B200:
-//   * Each 16-row block of the layer is a list of equal "chunks": the quantized
-//     part (256 K columns of codes per chunk, contiguous in the tile layout)
-//     followed by the weak block (64 fp16 columns per chunk, row-block tiles).
-//     grid = (S ranks, 128-row groups) launched as clusters of the S ranks of
-//     one row group; rank s takes an equal contiguous share of the chunk list,
-//     so quantized and weak work are balanced across the cluster.
-//   * CTA = 4 warps; warp w owns TWO row-blocks (32 rows) so every x fragment,
-//     every sum(x) MMA and all per-chunk bookkeeping is shared by 32 rows.
-//   * Chunks stream through shared memory with TMA bulk copies
-//     (cp.async.bulk + mbarrier complete_tx) into a private ring per warp; a
-//     quantized chunk's group (scale, zero) pairs ride in the same slot. One lane
-//     refills a slot as soon as the warp consumed it. The first ring-full is
-//     issued before the programmatic-dependent-launch wait, so a kernel's weight
-//     stream overlaps the previous kernel in the stream.
-//   * x is staged per chunk into a double-buffered smem tile by the whole CTA,
-//     prefetched one chunk ahead in registers.
-//   * codes become mma.m16n8k16 A fragments with one LOP3 per fragment
-//     ((magic + code) halves); the MMA accumulates sum (magic + c) x in fp32 and a
-//     second MMA with an all-ones A fragment accumulates sum(x) in the same
-//     fragment layout, so the per-group fold
+// HBM-bound design for B200 (one pass over the packed weights, nothing else):
+//   * The tile layout (qeft_common.cuh) hands every lane exactly the 16 bytes of
+//     a 16 x 64 tile that form its mma.m16n8k16 A fragments, so codes go
+//     straight from HBM into registers with coalesced 128-bit streaming loads
+//     (ld.global.nc.L1::no_allocate) -- no shared-memory staging. Measured on
+//     B200 (scripts/micro/stream_bench.cu): register streaming with >= 16
+//     warps/SM reaches 6.5-7 TB/s, while cp.async.bulk saturates at ~4 copies
+//     in flight per CTA (2-4 KB copies: 1.2-2.3 TB/s).
+//   * CTA = 8 warps on one row-block (16 output rows); the warps split the K
+//     range in whole groups, so every CTA owns complete output rows and the
+//     K-partials are summed in a fixed order through shared memory: no
+//     cross-CTA reduction, deterministic results.
+//   * Each warp software-pipelines its K range in batches of kU 64-column
+//     steps with incremental pointers and no bounds checks in the steady state:
+//     the next batch's codes and (scale, zero) pairs are in flight while the
+//     current batch is decoded and multiplied. The first batch is issued BEFORE
+//     the programmatic-dependent-launch wait, so a layer's weight stream
+//     overlaps the previous kernel; only x (staged once into shared memory in
+//     the B200 K order, zero padded) and the trainable weak block wait for it.
+//   * Codes become (magic + code) half2 A fragments with one LOP3 each; a
+//     second MMA with an all-ones A fragment yields sum(x) in the accumulator
+//     layout, so the per-group fold
 //       y += s' * acc + (z - magic * s') * sum(x)   (s' = s, or s/16 for the
-//     fp16 hi-nibble trick) needs no separate pass over x.
-//   * Ranks are combined deterministically through distributed shared memory:
-//     each CTA leaves its fp32 partial in its own smem, the cluster syncs, and
-//     rank 0 sums the ranks in order.
+//     fp16 hi-nibble trick) needs no separate pass over x. GT (64-column steps
+//     per group) is a template constant; GT = 0 is the generic per-element
+//     dequant path for group sizes that are not 64 * {1, 2, 4}.
 #include <algorithm>
+#include <cstdlib>
 
 #include "qeft_common.cuh"
 #include "qeft_internal.h"
@@ -38,35 +39,38 @@ using namespace qeft;
 
 namespace {
 
-constexpr int kWarps = 4;
+constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
-constexpr int kRB = 2;                // row-blocks per warp
-constexpr int kRows = kWarps * kRB * 16;  // rows per CTA
-constexpr int kSlots = 2;             // ring depth per warp (2 x 4 KB of codes in flight)
-constexpr int kQCols = 256;           // K columns per quantized chunk
-constexpr int kWCols = 64;            // K columns per weak chunk
-constexpr int kQBytes4 = 2048;        // 16 rows x 256 codes x 4 bit
-constexpr int kQBytes3 = 1536;        // 16 rows x 256 codes x 3 bit
-constexpr int kWBytes = 2048;         // 16 rows x 64 x 16 bit
-constexpr int kPart = 2560;           // per row-block: chunk bytes (<= 2 KB) + (s, z) of <= 4 groups
-constexpr int kSzOff = 2048;
-constexpr int kSlotBytes = kRB * kPart;
-constexpr int kMaxCluster = 8;
-constexpr int kXStride = kQCols + 8;  // halves; 528 B == 16 mod 32 -> conflict-free LDS.128
+constexpr int kU = 4;                 // 64-column steps per pipelined batch
+constexpr int kR = 4;                 // per-warp cp.async ring depth (batches)
+constexpr int kXSmemMax = 32 * 1024;  // stage x in smem up to this size, else read via L1
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
 
 struct GemvArgs {
   const uint8_t* qw;
   const float2* sz;
-  const void* weak16;
-  const void* x;      // [n][ldx]; fast: original columns; else pre-gathered B200 order
-  int64_t ldx;
+  const uint8_t* weak16;
+  const uint8_t* x;  // fast: original columns; else pre-gathered B200 order [n][m_pad + k_pad]
+  int64_t ldx;       // elements
   void* y;
   int64_t ldy;
   int y_f32;
-  int oc, m, m_pad, k, k_pad, g, ng, n;
-  int nq, nw, ranks, gathered;  // chunks per row-block: nq quantized + nw weak
-  int gt;                       // 64-column steps per group (FOLD: g % 64 == 0)
-  uint32_t mgt;                 // ceil(2^32 / gt): ti / gt == umulhi(ti, mgt) for gt > 1
+  int oc, m, m_pad, k, k_pad, g, ng, n, n_rb;
+  int gathered;
+  int nsq;      // quantized 64-column steps (m_pad / 64)
+  int spw;      // quantized steps per warp (multiple of the group's steps)
+  int xs_ld;    // smem x row stride (elements), 0 = x read through L1
+  int64_t rbb;  // qweight bytes per row-block
 };
 
 template <typename T>
@@ -77,161 +81,110 @@ __device__ __forceinline__ void store_out(const GemvArgs& a, int n, int row, flo
     ((T*)a.y)[(int64_t)n * a.ldy + row] = from_f32<T>(v);
 }
 
-template <int BITS, int NT, typename T, bool FOLD>
-__global__ void __launch_bounds__(kThreads)
-gemv_kernel(const GemvArgs a) {
-  using T2 = typename DTraits<T>::T2;
-  constexpr int kXPer = NT * 2;  // uint4 of x per thread per chunk: (8*NT rows x 256 cols / 8) / 128
-  constexpr int kQBytes = BITS == 4 ? kQBytes4 : kQBytes3;
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bars[kWarps][kSlots];
-  __shared__ __align__(16) float xsum_s[2][kQCols / 64][16];
-  float (*part)[kRows] = reinterpret_cast<float (*)[kRows]>(smem);  // reuses the rings at the end
+QEFT_DEV uint4 ldg_l1(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+QEFT_DEV float2 ldg_f2(const float2* p) {
+  float2 r;
+  asm volatile("ld.global.nc.v2.f32 {%0,%1}, [%2];\n" : "=f"(r.x), "=f"(r.y) : "l"(p));
+  return r;
+}
+QEFT_DEV uint32_t ldg_stream32(const void* p) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];\n" : "=r"(r) : "l"(p));
+  return r;
+}
 
-  const int s = blockIdx.x, rg = blockIdx.y;
+// x element (n, j) of the B200 K order (quantized [0, m_pad), weak [m_pad, m_pad + k_pad)),
+// 8 consecutive columns starting at j (j % 8 == 0); zero for padding
+template <typename T>
+QEFT_DEV uint4 x_chunk(const GemvArgs& a, int n, int j) {
+  if (a.gathered) return ldg_l1(reinterpret_cast<const T*>(a.x) + (int64_t)n * a.ldx + j);
+  int col;
+  if (j < a.m_pad) {
+    if (j >= a.m) return make_uint4(0, 0, 0, 0);
+    col = j;
+  } else {
+    const int w = j - a.m_pad;
+    if (w >= a.k) return make_uint4(0, 0, 0, 0);
+    col = a.m + w;
+  }
+  return ldg_l1(reinterpret_cast<const T*>(a.x) + (int64_t)n * a.ldx + col);
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+template <int GT>
+struct Ring {
+  static constexpr int G = GT > 0 ? GT : 1;
+  static constexpr int kSP = kU / G;                   // group-param slots per batch
+  static constexpr int kSlot = kU * 512 + kSP * 128;   // bytes per warp per batch
+};
+
+template <int BITS, int NT, int GT, typename T, bool XS>
+__global__ void __launch_bounds__(kThreads, 2)
+gemv_kernel(const GemvArgs a) {
+  // dynamic smem: [x (XS only): n x xs_ld][weak tiles: 2 x wbytes][rings: kWarps x kR x kSlot]
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ float part[2][kWarps][16][NT * 8];
+  __shared__ __align__(8) uint64_t wbar[2];
+  constexpr bool FOLD = GT > 0;
+  constexpr int G = Ring<GT>::G, kSP = Ring<GT>::kSP, kSlot = Ring<GT>::kSlot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g8 = lane >> 2, t4 = lane & 3;
-  const int rb0 = (rg * kWarps + warp) * kRB;           // first of this warp's row-blocks
-  const int nrb = min(kRB, max(0, (a.oc - rb0 * 16 + 15) / 16));  // valid row-blocks (0..2)
-  const int ntot = a.nq + a.nw;
-  const int c0 = (int)((int64_t)s * ntot / a.ranks), c1 = (int)((int64_t)(s + 1) * ntot / a.ranks);
-  const int nchunk = c1 - c0;
-  uint8_t* ring = smem + warp * (kSlots * kSlotBytes);
-  T* xs = reinterpret_cast<T*>(smem + kWarps * kSlots * kSlotBytes);  // [2][8*NT][kXStride]
-  uint64_t* bar = bars[warp];
-  const int64_t rbb = rowblock_bytes(BITS, a.m_pad);
+  const int s_beg = min(warp * a.spw, a.nsq), s_end = min(s_beg + a.spw, a.nsq);
+  const int nsteps = s_end - s_beg;
+  const int nb = (nsteps + kU - 1) / kU;  // batches per row-block (last may be partial)
+  // persistent: this CTA's row-blocks are blockIdx.x + j * gridDim.x
+  const int nrbc = (a.n_rb - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int nwt = a.k_pad >> 6;
+  const uint32_t wbytes = (uint32_t)nwt * 2048u;
+  uint8_t* wsm = smem + (XS ? (size_t)a.n * a.xs_ld * sizeof(T) : 0);
+  uint8_t* ring = wsm + 2 * wbytes + (size_t)warp * kR * kSlot;
 
-  // ti / gt without a hardware-emulated division (exact for ti * gt < 2^32)
-  auto div_gt = [&](int ti) -> int { return a.gt == 1 ? ti : (int)__umulhi((uint32_t)ti, a.mgt); };
+  auto rb_of = [&](int j) { return (int)blockIdx.x + j * (int)gridDim.x; };
 
-  // ---- 1. producer: lane 0 of each warp fills its private ring ----
-  auto issue = [&](int c, int slot) {
-    uint8_t* dst = ring + slot * kSlotBytes;
-    if (c >= a.nq) {
-      mbar_expect_tx(&bar[slot], nrb * kWBytes);
-      for (int r = 0; r < nrb; ++r)
-        bulk_g2s(dst + r * kPart,
-                 (const uint8_t*)a.weak16 + ((int64_t)(rb0 + r) * (a.k_pad >> 6) + (c - a.nq)) * kWBytes,
-                 kWBytes, &bar[slot]);
-      return;
-    }
-    const int tiles = min(kQCols, a.m_pad - c * kQCols) >> 6;
-    const uint32_t nb = (uint32_t)(tiles * 64 * 2 * BITS);  // 16 rows * bits / 8 per column
-    int gf = 0;
-    uint32_t nsz = 0;
-    if (FOLD) {
-      gf = min(div_gt(c * (kQCols / 64)), a.ng - 1);
-      const int gl = min(div_gt(c * (kQCols / 64) + tiles - 1), a.ng - 1);
-      nsz = (uint32_t)(gl - gf + 1) * 16 * sizeof(float2);
-    }
-    mbar_expect_tx(&bar[slot], nrb * (nb + nsz));
-    for (int r = 0; r < nrb; ++r) {
-      bulk_g2s(dst + r * kPart, a.qw + (int64_t)(rb0 + r) * rbb + (int64_t)c * kQBytes, nb, &bar[slot]);
-      if (FOLD)
-        bulk_g2s(dst + r * kPart + kSzOff, a.sz + ((int64_t)(rb0 + r) * a.ng + gf) * 16, nsz, &bar[slot]);
-    }
-  };
-  if (lane == 0) {
-    for (int i = 0; i < kSlots; ++i) mbar_init(&bar[i], 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-  if (lane == 0 && nrb > 0) {
-    for (int i = 0; i < min(nchunk, kSlots); ++i) issue(c0 + i, i);
-  }
-
-  // Programmatic dependent launch: the next kernel may start streaming its own
-  // weights now; x (the previous kernel's output) is read only after the wait.
-  pdl_launch_dependents();
-  pdl_wait();
-
-  // x chunk staging: thread -> (row xn, 8-column piece xp) pairs, kXPer per thread
-  auto cbase = [&](int c) { return c < a.nq ? c * kQCols : a.m_pad + (c - a.nq) * kWCols; };
-  const T* xg = (const T*)a.x;
-  uint4 xr[kXPer];
-  auto x_load = [&](int c) {
-    const int base = cbase(c);
-    const int lim = c < a.nq ? a.m : a.m_pad + a.k;  // valid B200 columns of this region
-#pragma unroll
-    for (int i = 0; i < kXPer; ++i) {
-      const int e = threadIdx.x + i * kThreads;
-      const int n = e >> 5, j = base + 8 * (e & 31);
-      const int col = (a.gathered || j < a.m_pad) ? j : a.m + (j - a.m_pad);
-      const bool ok = n < a.n && (a.gathered ? (j < a.m_pad + a.k_pad) : (j < lim)) &&
-                      (c >= a.nq ? (8 * (e & 31) < kWCols) : true);
-      xr[i] = ok ? *reinterpret_cast<const uint4*>(xg + (int64_t)n * a.ldx + col) : make_uint4(0, 0, 0, 0);
-    }
-  };
-  // also leaves fp32 sums of every 64-column segment: xsum_s[buf][seg][row] (zero-point fold)
-  auto x_store = [&](int buf) {
-#pragma unroll
-    for (int i = 0; i < kXPer; ++i) {
-      const int e = threadIdx.x + i * kThreads;
-      *reinterpret_cast<uint4*>(xs + (buf * 8 * NT + (e >> 5)) * kXStride + 8 * (e & 31)) = xr[i];
-      if constexpr (FOLD) {
-        const T2* h = reinterpret_cast<const T2*>(&xr[i]);
-        float sum = 0.f;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float2 f2 = t2_to_f2<T2>(h[q]);
-          sum += f2.x + f2.y;
-        }
-        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-        sum += __shfl_xor_sync(0xffffffffu, sum, 4);
-        if ((lane & 7) == 0) xsum_s[buf][(e & 31) >> 3][e >> 5] = sum;
-      }
-    }
-  };
-  if (nchunk > 0) {
-    x_load(c0);
-    x_store(0);
-  }
-  __syncthreads();
-
-  float acc[kRB][NT][4], accg[kRB][NT][4], accx[NT][4];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      accx[nt][e] = 0.f;
-#pragma unroll
-      for (int r = 0; r < kRB; ++r) acc[r][nt][e] = accg[r][nt][e] = 0.f;
-    }
-  const uint32_t ones[4] = {DTraits<T>::kOne2, DTraits<T>::kOne2, DTraits<T>::kOne2, DTraits<T>::kOne2};
-  int xrow[NT];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) xrow[nt] = min(g8 + 8 * nt, a.n - 1);
-
-  // fold group grp of row-block r; its params are in the current slot (starting at group gf)
-  auto fold = [&](int grp, const uint8_t* buf, int gf) {
-    constexpr float M = DTraits<T>::kMagicF;
-#pragma unroll
-    for (int r = 0; r < kRB; ++r) {
-      const float2* sz = reinterpret_cast<const float2*>(buf + r * kPart + kSzOff) + (grp - gf) * 16;
-      const float2 p0 = sz[g8];
-      const float2 p1 = sz[g8 + 8];
-      const float s0 = p0.x;
-      const float s1 = (BITS == 4 && DTraits<T>::kHiTrick) ? p1.x * (1.f / 16.f) : p1.x;
-      const float z0 = p0.y - M * s0, z1 = p1.y - M * s1;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        acc[r][nt][0] += s0 * accg[r][nt][0] + z0 * accx[nt][0];
-        acc[r][nt][1] += s0 * accg[r][nt][1] + z0 * accx[nt][1];
-        acc[r][nt][2] += s1 * accg[r][nt][2] + z1 * accx[nt][2];
-        acc[r][nt][3] += s1 * accg[r][nt][3] + z1 * accx[nt][3];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) accg[r][nt][e] = 0.f;
-      }
-    }
+  float acc[NT][4], accg[NT][4], accx[NT][4];
+  auto zero_acc = [&]() {
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) accx[nt][e] = 0.f;
+      for (int e = 0; e < 4; ++e) acc[nt][e] = accg[nt][e] = accx[nt][e] = 0.f;
   };
+  zero_acc();
+  int xrow[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) xrow[nt] = min(g8 + 8 * nt, a.n - 1);
+  const uint32_t ones[4] = {DTraits<T>::kOne2, DTraits<T>::kOne2, DTraits<T>::kOne2, DTraits<T>::kOne2};
 
-  // per-element dequant (group sizes that are not a multiple of 64)
-  auto dq_frag = [&](uint32_t mag, bool hi16, int rb, int row_local, int col) -> uint32_t {
+  auto bsel = [](const uint4& xa, const uint4& xb, int j, uint32_t& b0, uint32_t& b1) {
+    b0 = (j == 0) ? xa.x : (j == 1) ? xa.z : (j == 2) ? xb.x : xb.z;
+    b1 = (j == 0) ? xa.y : (j == 1) ? xa.w : (j == 2) ? xb.y : xb.w;
+  };
+  // B fragments of the 64-column step starting at B200 K position j
+  auto x_frag = [&](int j, uint4 xa[NT], uint4 xb[NT]) {
+    const int c0 = j + 16 * t4;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      if constexpr (XS) {
+        const T* xp = reinterpret_cast<const T*>(smem) + xrow[nt] * a.xs_ld + c0;
+        xa[nt] = *reinterpret_cast<const uint4*>(xp);
+        xb[nt] = *reinterpret_cast<const uint4*>(xp + 8);
+      } else {
+        xa[nt] = x_chunk<T>(a, xrow[nt], c0);
+        xb[nt] = x_chunk<T>(a, xrow[nt], c0 + 8);
+      }
+    }
+  };
+  // per-element dequant for group sizes that are not 64 * {1, 2, 4}
+  auto dq_frag = [&](int rb, uint32_t mag, bool hi16, int row_local, int col) -> uint32_t {
+    using T2 = typename DTraits<T>::T2;
     const float2 cf = t2_to_f2<T2>(magic_to_code<T>(mag, hi16));
     const int gA = min(col / a.g, a.ng - 1), gB = min((col + 1) / a.g, a.ng - 1);
     const float2* sz = a.sz + (int64_t)rb * a.ng * 16;
@@ -243,210 +196,265 @@ gemv_kernel(const GemvArgs a) {
     return *reinterpret_cast<uint32_t*>(&r);
   };
 
-  // B fragments of one 64-column step at chunk-local column xc
-  auto x_frag = [&](const T* xbuf, int xc, uint4 xa[NT], uint4 xb[NT]) {
+  // one 64-column step: decode + MMA (+ fold with params p0/p1 when `fold_now`)
+  auto step = [&](int rb, int st, const uint4& q, const float2* szs, bool fold_now) {
+    const int col = st * 64;
+    uint4 xa[NT], xb[NT];
+    x_frag(col, xa, xb);
+    if constexpr (FOLD) {
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const T* xp = xbuf + xrow[nt] * kXStride + xc + 16 * t4;
-      xa[nt] = *reinterpret_cast<const uint4*>(xp);
-      xb[nt] = *reinterpret_cast<const uint4*>(xp + 8);
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          uint32_t b0_, b1_;
+          bsel(xa[nt], xb[nt], j, b0_, b1_);
+          mma16816<T>(accx[nt], ones, b0_, b1_);
+        }
+    }
+    uint32_t f[4][4];
+    if constexpr (BITS == 4) {
+      const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) decode4<T>(qq[j], f[j]);
+    } else {
+      const uint32_t ww2[2] = {q.x, q.y};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) f[j][pp] = decode3_pair<T>(ww2[j >> 1], q.z, 4 * (j & 1) + pp, j >> 1);
+    }
+    if constexpr (!FOLD) {
+      constexpr bool h16 = (BITS == 4) && DTraits<T>::kHiTrick;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int cc = col + 16 * t4 + 4 * j;
+        f[j][0] = dq_frag(rb, f[j][0], false, g8, cc);
+        f[j][1] = dq_frag(rb, f[j][1], h16, g8 + 8, cc);
+        f[j][2] = dq_frag(rb, f[j][2], false, g8, cc + 2);
+        f[j][3] = dq_frag(rb, f[j][3], h16, g8 + 8, cc + 2);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        uint32_t b0_, b1_;
+        bsel(xa[nt], xb[nt], j, b0_, b1_);
+        mma16816<T>(FOLD ? accg[nt] : acc[nt], f[j], b0_, b1_);
+      }
+    if constexpr (FOLD) {
+      if (fold_now) {
+        constexpr float M = DTraits<T>::kMagicF;
+        const float2 p0 = szs[g8], p1 = szs[g8 + 8];
+        const float s0 = p0.x;
+        const float s1 = (BITS == 4 && DTraits<T>::kHiTrick) ? p1.x * (1.f / 16.f) : p1.x;
+        const float z0 = p0.y - M * s0, z1 = p1.y - M * s1;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          acc[nt][0] += s0 * accg[nt][0] + z0 * accx[nt][0];
+          acc[nt][1] += s0 * accg[nt][1] + z0 * accx[nt][1];
+          acc[nt][2] += s1 * accg[nt][2] + z1 * accx[nt][2];
+          acc[nt][3] += s1 * accg[nt][3] + z1 * accx[nt][3];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) accg[nt][e] = accx[nt][e] = 0.f;
+        }
+      }
     }
   };
-  auto bsel = [](const uint4& xa, const uint4& xb, int j, uint32_t& b0, uint32_t& b1) {
-    b0 = (j == 0) ? xa.x : (j == 1) ? xa.z : (j == 2) ? xb.x : xb.z;
-    b1 = (j == 0) ? xa.y : (j == 1) ? xa.w : (j == 2) ? xb.y : xb.w;
-  };
 
-  // last quantized column this rank covers (a group is folded at its end or here)
-  const int qend = min(min(c1, a.nq) * kQCols, a.m_pad);
-
-  // ---- 2. consumer: the CTA walks its chunks in lockstep (x is shared) ----
-  for (int i = 0; i < nchunk; ++i) {
-    const int c = c0 + i;
-    if (i + 1 < nchunk) x_load(c + 1);  // next x chunk in flight during this chunk's math
-    const T* xbuf = xs + (i & 1) * 8 * NT * kXStride;
-    if (nrb > 0) {
-      const int slot = i % kSlots;
-      mbar_wait(&bar[slot], (i / kSlots) & 1);
-      const uint8_t* buf = ring + slot * kSlotBytes;
-      if (c >= a.nq) {
-        // weak tile: 16 rows x 64 fp16, row-major; lane reads rows g8, g8+8, cols 16t..16t+15
-        uint4 xa[NT], xb[NT];
-        x_frag(xbuf, 0, xa, xb);
+  // ---- the warp's batch stream through its private cp.async ring ----
+  // batch (row-block j, batch b) = kU 64-column steps; every step of a group slot
+  // shares its group (batches start at group boundaries)
+  const int TB = nb * nrbc;
+  int ij = 0, ib = 0;
+  auto issue_next = [&](int t) {
+    if (t < TB) {
+      uint8_t* slot = ring + (t % kR) * kSlot;
+      const int rb = rb_of(ij);
+      const int b0 = s_beg + ib * kU;
+      const uint8_t* base = a.qw + rb * a.rbb;
 #pragma unroll
-        for (int r = 0; r < kRB; ++r) {
-          const T* w16 = (const T*)(buf + r * kPart);
-          const uint4 r0a = *reinterpret_cast<const uint4*>(w16 + g8 * 64 + 16 * t4);
-          const uint4 r0b = *reinterpret_cast<const uint4*>(w16 + g8 * 64 + 16 * t4 + 8);
-          const uint4 r1a = *reinterpret_cast<const uint4*>(w16 + (g8 + 8) * 64 + 16 * t4);
-          const uint4 r1b = *reinterpret_cast<const uint4*>(w16 + (g8 + 8) * 64 + 16 * t4 + 8);
-          const uint32_t f[4][4] = {{r0a.x, r1a.x, r0a.y, r1a.y}, {r0a.z, r1a.z, r0a.w, r1a.w},
-                                    {r0b.x, r1b.x, r0b.y, r1b.y}, {r0b.z, r1b.z, r0b.w, r1b.w}};
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-              uint32_t b0, b1;
-              bsel(xa[nt], xb[nt], j, b0, b1);
-              mma16816<T>(acc[r][nt], f[j], b0, b1);
-            }
-        }
-      } else {
-        const int jc0 = c * kQCols;
-        const int tiles = min(kQCols, a.m_pad - jc0) >> 6;
-        // group bookkeeping without per-step division
-        const int t0 = c * (kQCols / 64);
-        int grp = FOLD ? div_gt(t0) : 0;
-        const int gf = FOLD ? min(grp, a.ng - 1) : 0;
-        int left = FOLD ? a.gt - (t0 - grp * a.gt) : 0;
-#pragma unroll
-        for (int st = 0; st < kQCols / 64; ++st) {
-          if (st < tiles) {
-            const int jc = jc0 + 64 * st;
-            uint4 xa[NT], xb[NT];
-            x_frag(xbuf, 64 * st, xa, xb);
-            // sum(x) of this step for this lane's output columns (2t, 2t+1 [+8])
-            if constexpr (FOLD) {
-#pragma unroll
-              for (int nt = 0; nt < NT; ++nt) {
-                const float2 sx = *reinterpret_cast<const float2*>(&xsum_s[i & 1][st][8 * nt + 2 * t4]);
-                accx[nt][0] += sx.x;
-                accx[nt][1] += sx.y;
-                accx[nt][2] += sx.x;
-                accx[nt][3] += sx.y;
-              }
-            }
-#pragma unroll
-            for (int r = 0; r < kRB; ++r) {
-              uint32_t f[4][4];
-              if constexpr (BITS == 4) {
-                const uint4 q = *reinterpret_cast<const uint4*>(buf + r * kPart + st * 512 + lane * 16);
-                const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) decode4<T>(qq[j], f[j]);
-              } else {
-                const uint8_t* tb = buf + r * kPart + (st >> 1) * 768;
-                const int h = st & 1;
-                const uint2 w2 = *reinterpret_cast<const uint2*>(tb + lane * 16 + 8 * h);
-                const uint32_t hb = *reinterpret_cast<const uint32_t*>(tb + 512 + lane * 8 + 4 * h);
-                const uint32_t ww2[2] = {w2.x, w2.y};
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-#pragma unroll
-                  for (int pp = 0; pp < 4; ++pp)
-                    f[j][pp] = decode3_pair<T>(ww2[j >> 1], hb, 4 * (j & 1) + pp, j >> 1);
-              }
-              if constexpr (!FOLD) {
-                constexpr bool h16 = (BITS == 4) && DTraits<T>::kHiTrick;
-                const int rb = rb0 + r;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  const int cc = jc + 16 * t4 + 4 * j;
-                  f[j][0] = dq_frag(f[j][0], false, rb, g8, cc);
-                  f[j][1] = dq_frag(f[j][1], h16, rb, g8 + 8, cc);
-                  f[j][2] = dq_frag(f[j][2], false, rb, g8, cc + 2);
-                  f[j][3] = dq_frag(f[j][3], h16, rb, g8 + 8, cc + 2);
-                }
-              }
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt) {
-                  uint32_t b0, b1;
-                  bsel(xa[nt], xb[nt], j, b0, b1);
-                  mma16816<T>(FOLD ? accg[r][nt] : acc[r][nt], f[j], b0, b1);
-                }
-            }
-            if constexpr (FOLD) {
-              // a group is folded right after its last step, while its params are in this slot
-              if (--left == 0 || jc + 64 >= qend) {
-                fold(min(grp, a.ng - 1), buf, gf);
-                ++grp;
-                left = a.gt;
-              }
-            }
+      for (int u = 0; u < kU; ++u) {
+        const int st = b0 + u;
+        if (st < s_end) {
+          if constexpr (BITS == 4) {
+            cp_async16(slot + u * 512 + lane * 16, base + (int64_t)st * 512 + lane * 16);
+          } else {
+            const uint8_t* tb = base + (int64_t)(st >> 1) * 768;
+            const int h = st & 1;
+            cp_async8(slot + u * 512 + lane * 16, tb + lane * 16 + 8 * h);
+            cp_async4(slot + u * 512 + lane * 16 + 8, tb + 512 + lane * 8 + 4 * h);
           }
         }
       }
-      // slot consumed by the whole warp -> refill it
-      __syncwarp();
-      if (lane == 0 && i + kSlots < nchunk) issue(c + kSlots, slot);
-    }
-    if (i + 1 < nchunk) x_store((i + 1) & 1);
-    __syncthreads();
-  }
-
-  // ---- 3. output ----
-  if (a.ranks == 1) {
+      if (FOLD && lane < 16) {
+        const float2* szp = a.sz + ((int64_t)rb * a.ng) * 16 + lane;
 #pragma unroll
-    for (int r = 0; r < kRB; ++r) {
-      const int row0 = (rb0 + r) * 16 + g8, row1 = row0 + 8;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int cA = 8 * nt + 2 * t4;
-        if (cA < a.n) {
-          if (row0 < a.oc) store_out<T>(a, cA, row0, acc[r][nt][0]);
-          if (row1 < a.oc) store_out<T>(a, cA, row1, acc[r][nt][2]);
-        }
-        if (cA + 1 < a.n) {
-          if (row0 < a.oc) store_out<T>(a, cA + 1, row0, acc[r][nt][1]);
-          if (row1 < a.oc) store_out<T>(a, cA + 1, row1, acc[r][nt][3]);
+        for (int i = 0; i < kSP; ++i) {
+          if (b0 + i * G < s_end) {
+            const int grp = min(b0 / G + i, a.ng - 1);
+            cp_async8(slot + kU * 512 + i * 128 + lane * 8, szp + grp * 16);
+          }
         }
       }
+      if (++ib == nb) { ib = 0; ++ij; }
     }
-    return;
-  }
-  __syncthreads();  // every warp is done with its ring before partials overwrite it
+    cp_async_commit();  // one group per batch (possibly empty) keeps the wait count uniform
+  };
+  auto compute = [&](int t, int j, int b) {
+    const uint8_t* slot = ring + (t % kR) * kSlot;
+    const int rb = rb_of(j);
+    const int b0 = s_beg + b * kU;
 #pragma unroll
-  for (int r = 0; r < kRB; ++r) {
-    const int rl0 = (warp * kRB + r) * 16 + g8, rl1 = rl0 + 8;
+    for (int u = 0; u < kU; ++u) {
+      const int st = b0 + u;
+      if (st < s_end) {
+        const uint4 q = *reinterpret_cast<const uint4*>(slot + u * 512 + lane * 16);
+        const float2* szs = reinterpret_cast<const float2*>(slot + kU * 512 + (u / G) * 128);
+        step(rb, st, q, szs, (u % G) == G - 1 || st + 1 == s_end);
+      }
+    }
+  };
+
+  if (threadIdx.x == 0) {
+    mbar_init(&wbar[0], 1);
+    mbar_init(&wbar[1], 1);
+    fence_mbar_init();
+  }
+#pragma unroll
+  for (int t = 0; t < kR - 1; ++t) issue_next(t);
+  // Programmatic dependent launch: the next layer may start streaming its weights
+  // now; x (the previous kernel's output) and the trainable weak block are read
+  // after the wait.
+  pdl_launch_dependents();
+  pdl_wait();
+  __syncthreads();  // barrier init visible
+  auto issue_weak = [&](int j) {
+    if (nwt > 0 && j < nrbc) {
+      mbar_expect_tx(&wbar[j & 1], wbytes);
+      bulk_g2s(wsm + (j & 1) * wbytes, a.weak16 + (int64_t)rb_of(j) * wbytes, wbytes, &wbar[j & 1]);
+    }
+  };
+  if (threadIdx.x == 0) {
+    issue_weak(0);
+    issue_weak(1);
+  }
+  if constexpr (XS) {
+    const int row_chunks = (a.m_pad + a.k_pad) >> 3;
+    for (int e = threadIdx.x; e < a.n * row_chunks; e += kThreads) {
+      const int n = e / row_chunks, jj = (e - n * row_chunks) << 3;
+      *reinterpret_cast<uint4*>(reinterpret_cast<T*>(smem) + n * a.xs_ld + jj) = x_chunk<T>(a, n, jj);
+    }
+    __syncthreads();
+  }
+  // weak tiles + fixed-order sum of the warps' K-partials for row-block j
+  // (part is double-buffered: one barrier per row-block)
+  auto finish = [&](int j) {
+    const int rb = rb_of(j);
+    if (warp < nwt) mbar_wait(&wbar[j & 1], (j >> 1) & 1);
+    for (int wt = warp; wt < nwt; wt += kWarps) {
+      const T* w16 = reinterpret_cast<const T*>(wsm + (j & 1) * wbytes) + wt * 1024;
+      const uint4 r0a = *reinterpret_cast<const uint4*>(w16 + g8 * 64 + 16 * t4);
+      const uint4 r0b = *reinterpret_cast<const uint4*>(w16 + g8 * 64 + 16 * t4 + 8);
+      const uint4 r1a = *reinterpret_cast<const uint4*>(w16 + (g8 + 8) * 64 + 16 * t4);
+      const uint4 r1b = *reinterpret_cast<const uint4*>(w16 + (g8 + 8) * 64 + 16 * t4 + 8);
+      uint4 xa[NT], xb[NT];
+      x_frag(a.m_pad + wt * 64, xa, xb);
+      const uint32_t f[4][4] = {{r0a.x, r1a.x, r0a.y, r1a.y}, {r0a.z, r1a.z, r0a.w, r1a.w},
+                                {r0b.x, r1b.x, r0b.y, r1b.y}, {r0b.z, r1b.z, r0b.w, r1b.w}};
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          uint32_t b0_, b1_;
+          bsel(xa[nt], xb[nt], jj, b0_, b1_);
+          mma16816<T>(acc[nt], f[jj], b0_, b1_);
+        }
+    }
+    float (*pp)[16][NT * 8] = part[j & 1];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int cA = 8 * nt + 2 * t4;
-      part[cA][rl0] = acc[r][nt][0];
-      part[cA][rl1] = acc[r][nt][2];
-      part[cA + 1][rl0] = acc[r][nt][1];
-      part[cA + 1][rl1] = acc[r][nt][3];
+      pp[warp][g8][cA] = acc[nt][0];
+      pp[warp][g8][cA + 1] = acc[nt][1];
+      pp[warp][g8 + 8][cA] = acc[nt][2];
+      pp[warp][g8 + 8][cA + 1] = acc[nt][3];
     }
-  }
-  cluster_sync();  // partials of every rank are visible cluster-wide
-  if (cluster_ctarank() == 0) {
-    const uint32_t local = smem_u32(&part[0][0]);
-    for (int e = threadIdx.x; e < a.n * kRows; e += blockDim.x) {
-      const int cc = e / kRows, rl = e % kRows;
+    zero_acc();
+    __syncthreads();
+    // every warp is past row-block j's weak tiles: refill that buffer for j + 2
+    if (threadIdx.x == 0) issue_weak(j + 2);
+    for (int e = threadIdx.x; e < 16 * a.n; e += kThreads) {
+      const int rl = e & 15, n = e >> 4;
       float v = 0.f;
-      for (int r = 0; r < a.ranks; ++r) v += ld_dsmem_f32(local + (uint32_t)(cc * kRows + rl) * 4, r);
-      const int row = rg * kRows + rl;
-      if (row < a.oc) store_out<T>(a, cc, row, v);
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) v += pp[w][rl][n];
+      const int row = rb * 16 + rl;
+      if (row < a.oc) store_out<T>(a, n, row, v);
+    }
+  };
+
+  if (nb == 0) {
+    for (int j = 0; j < nrbc; ++j) finish(j);
+    return;
+  }
+  int cj = 0, cb = 0;
+  for (int t = 0; t < TB; ++t) {
+    cp_async_wait<kR - 2>();  // batch t has landed (this lane's copies)
+    __syncwarp();             // ... and every lane's (group params are shared)
+    compute(t, cj, cb);
+    issue_next(t + kR - 1);   // refills the slot consumed at t - 1
+    if (++cb == nb) {
+      finish(cj);
+      cb = 0;
+      ++cj;
     }
   }
-  cluster_sync();  // keep every rank's smem alive until rank 0 has read it
 }
 
-template <int BITS, int NT, typename T, bool FOLD>
-int launch(const GemvArgs& a, int n_rg, cudaStream_t st) {
-  auto kern = gemv_kernel<BITS, NT, T, FOLD>;
-  const size_t smem = (size_t)kWarps * kSlots * kSlotBytes + (size_t)2 * 8 * NT * kXStride * sizeof(T);
-  static bool attr_done = false;
-  if (!attr_done) {
-    QEFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_done = true;
+template <int BITS, int NT, int GT, typename T>
+int launch(const GemvArgs& a0, cudaStream_t st) {
+  GemvArgs a = a0;
+  const size_t xs_bytes = (size_t)a.n * (a.m_pad + a.k_pad + 8) * sizeof(T);
+  const size_t w_bytes = (size_t)2 * (a.k_pad / 64) * 2048;
+  const size_t ring_bytes = (size_t)kWarps * kR * Ring<GT>::kSlot;
+  const bool xs = xs_bytes <= (size_t)kXSmemMax;
+  a.xs_ld = xs ? a.m_pad + a.k_pad + 8 : 0;  // 16 B skew between rows: conflict-free LDS.128
+  const size_t smem = (xs ? xs_bytes : 0) + w_bytes + ring_bytes;
+  QEFT_CHECK(smem <= 200 * 1024, QEFT_ERR_LAYOUT, "gemv: k_pad=%d too large", a.k_pad);
+  // persistent CTAs: as many per SM as shared memory allows (<= 2: registers),
+  // equal row-block counts per CTA
+  int per_sm = smem * 2 + 2 * 9 * 1024 <= 227 * 1024 ? 2 : 1;
+  per_sm = std::min(per_sm, env_int("QEFT_GEMV_CPS", per_sm));
+  const int slots = per_sm * num_sms();
+  const int per = (a.n_rb + slots - 1) / slots;
+  const int grid = (a.n_rb + per - 1) / per;
+  auto kern = xs ? gemv_kernel<BITS, NT, GT, T, true> : gemv_kernel<BITS, NT, GT, T, false>;
+  static bool attr[2] = {false, false};
+  if (!attr[xs]) {
+    QEFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr[xs] = true;
   }
-  QEFT_CUDA(launch_pdl_cluster(kern, dim3(a.ranks, n_rg), dim3(kThreads), smem, st, a.ranks, a));
+  QEFT_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, a));
   return 0;
 }
 
-template <typename T>
-int dispatch(const GemvArgs& a, int bits, int n_rg, bool fold, cudaStream_t st) {
+template <int BITS, typename T>
+int dispatch_gt(const GemvArgs& a, int gt, cudaStream_t st) {
   const bool nt2 = a.n > 8;
-#define QEFT_GEMV_CASE(B, NT, F) \
-  if (bits == B && (NT == 2) == nt2 && fold == F) return launch<B, NT, T, F>(a, n_rg, st);
-  QEFT_GEMV_CASE(4, 1, true) QEFT_GEMV_CASE(4, 2, true) QEFT_GEMV_CASE(4, 1, false)
-  QEFT_GEMV_CASE(4, 2, false) QEFT_GEMV_CASE(3, 1, true) QEFT_GEMV_CASE(3, 2, true)
-  QEFT_GEMV_CASE(3, 1, false) QEFT_GEMV_CASE(3, 2, false)
-#undef QEFT_GEMV_CASE
-  set_error("gemv: unsupported bits=%d", bits);
-  return QEFT_ERR_LAYOUT;
+#define QEFT_GT(NT)                                      \
+  switch (gt) {                                          \
+    case 1: return launch<BITS, NT, 1, T>(a, st);        \
+    case 2: return launch<BITS, NT, 2, T>(a, st);        \
+    case 4: return launch<BITS, NT, 4, T>(a, st);        \
+    default: return launch<BITS, NT, 0, T>(a, st);       \
+  }
+  if (nt2) {
+    QEFT_GT(2)
+  } else {
+    QEFT_GT(1)
+  }
+#undef QEFT_GT
 }
 
 }  // namespace
@@ -463,41 +471,44 @@ int gemv(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ld
   QEFT_CHECK(n >= 1 && n <= 16, QEFT_ERR_SHAPE, "gemv: n_cols=%d outside 1..16", n);
   QEFT_CHECK(L->bits == 3 || L->bits == 4, QEFT_ERR_SHAPE, "gemv: bits=%d", L->bits);
   QEFT_CHECK(ldx >= L->ic && ldy >= L->oc, QEFT_ERR_SHAPE, "gemv: ld too small");
-  GemvArgs a;
+  GemvArgs a{};
   a.qw = (const uint8_t*)L->qweight;
   a.sz = (const float2*)L->sz;
-  a.weak16 = L->weak16;
-  a.x = x;
-  a.ldx = ldx;
+  a.weak16 = (const uint8_t*)L->weak16;
   a.y = y;
   a.ldy = ldy;
   a.y_f32 = y_f32;
   a.oc = L->oc; a.m = L->m; a.m_pad = L->m_pad; a.k = L->k; a.k_pad = L->k_pad;
   a.g = L->g; a.ng = L->ng; a.n = n;
-  a.nq = (L->m_pad + kQCols - 1) / kQCols;
-  a.nw = L->k_pad / kWCols;
-  a.gt = std::max(1, L->g / 64);
-  a.mgt = a.gt > 1 ? (uint32_t)((0x100000000ull + a.gt - 1) / a.gt) : 0u;
-  const int n_rg = (L->oc_pad + kRows - 1) / kRows;
-  // ranks per row group: cover the chip ~2x, <= one portable cluster, >= 2 chunks each
-  int ranks = (2 * 148 + n_rg - 1) / n_rg;
-  ranks = std::min(ranks, kMaxCluster);
-  ranks = std::min(ranks, std::max(1, (a.nq + a.nw) / 2));
-  a.ranks = std::max(ranks, 1);
+  a.n_rb = L->oc_pad / 16;
+  a.rbb = rowblock_bytes(L->bits, L->m_pad);
+  a.nsq = L->m_pad / 64;
+  int gt = (L->g % 64) == 0 ? L->g / 64 : 0;
+  if (gt != 1 && gt != 2 && gt != 4) gt = 0;  // generic per-element dequant
+  // warps split the quantized steps in whole groups (and whole 3-bit tiles)
+  int unit = std::max(gt, 1);
+  if (L->bits == 3 && unit == 1) unit = 2;
+  int spw = (a.nsq + kWarps - 1) / kWarps;
+  spw = (spw + unit - 1) / unit * unit;
+  a.spw = std::max(spw, unit);
   const bool fast = (L->flags & QEFT_FLAG_STRUCTURED_FAST) && (ldx % 8 == 0) &&
                     (((uintptr_t)x & 15) == 0);
-  a.gathered = fast ? 0 : 1;
-  if (!fast) {
+  if (fast) {
+    a.x = (const uint8_t*)x;
+    a.ldx = ldx;
+    a.gathered = 0;
+  } else {
     const int kk = L->m_pad + L->k_pad;
     QEFT_CHECK(ws_bytes >= (size_t)n * kk * 2, QEFT_ERR_SHAPE, "gemv: workspace %zu too small",
                ws_bytes);
     if (int r = gather_cols(x, ldx, L->colmap, kk, n, L->act_dtype, ws, st)) return r;
-    a.x = ws;
+    a.x = (const uint8_t*)ws;
     a.ldx = kk;
+    a.gathered = 1;
   }
-  const bool fold = (L->g % 64) == 0;
-  if (L->act_dtype == QEFT_F16) return dispatch<__half>(a, L->bits, n_rg, fold, st);
-  return dispatch<__nv_bfloat16>(a, L->bits, n_rg, fold, st);
+  const bool bf = L->act_dtype == QEFT_BF16;
+  if (L->bits == 4) return bf ? dispatch_gt<4, __nv_bfloat16>(a, gt, st) : dispatch_gt<4, __half>(a, gt, st);
+  return bf ? dispatch_gt<3, __nv_bfloat16>(a, gt, st) : dispatch_gt<3, __half>(a, gt, st);
 }
 
 }  // namespace qeft
