@@ -71,6 +71,7 @@ struct GemvArgs {
   int spw;      // quantized steps per warp (multiple of the group's steps)
   int xs_ld;    // smem x row stride (elements), 0 = x read through L1
   int64_t rbb;  // qweight bytes per row-block
+  int dbg;      // tuning only: 1 = skip the weight stream (compute-only timing)
 };
 
 template <typename T>
@@ -268,7 +269,7 @@ gemv_kernel(const GemvArgs a) {
   const int TB = nb * nrbc;
   int ij = 0, ib = 0;
   auto issue_next = [&](int t) {
-    if (t < TB) {
+    if (t < TB && !a.dbg) {
       uint8_t* slot = ring + (t % kR) * kSlot;
       const int rb = rb_of(ij);
       const int b0 = s_beg + ib * kU;
@@ -301,10 +302,105 @@ gemv_kernel(const GemvArgs a) {
     }
     cp_async_commit();  // one group per batch (possibly empty) keeps the wait count uniform
   };
+  // decode the step's codes into mma A fragments ((magic + code) halves, or dequantized
+  // values on the generic path)
+  auto decode = [&](int rb, int st, const uint4& q, uint32_t (&f)[4][4]) {
+    if constexpr (BITS == 4) {
+      const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) decode4<T>(qq[j], f[j]);
+    } else {
+      const uint32_t ww2[2] = {q.x, q.y};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) f[j][pp] = decode3_pair<T>(ww2[j >> 1], q.z, 4 * (j & 1) + pp, j >> 1);
+    }
+    if constexpr (!FOLD) {
+      constexpr bool h16 = (BITS == 4) && DTraits<T>::kHiTrick;
+      const int col = st * 64;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int cc = col + 16 * t4 + 4 * j;
+        f[j][0] = dq_frag(rb, f[j][0], false, g8, cc);
+        f[j][1] = dq_frag(rb, f[j][1], h16, g8 + 8, cc);
+        f[j][2] = dq_frag(rb, f[j][2], false, g8, cc + 2);
+        f[j][3] = dq_frag(rb, f[j][3], h16, g8 + 8, cc + 2);
+      }
+    }
+  };
+  // fold group partials (g = sum (magic + c) x, xs = sum x) with the group's params
+  auto fold = [&](const float2* szs, const float (&g)[NT][4], const float (&xs)[NT][4]) {
+    constexpr float M = DTraits<T>::kMagicF;
+    const float2 p0 = szs[g8], p1 = szs[g8 + 8];
+    const float s0 = p0.x;
+    const float s1 = (BITS == 4 && DTraits<T>::kHiTrick) ? p1.x * (1.f / 16.f) : p1.x;
+    const float z0 = p0.y - M * s0, z1 = p1.y - M * s1;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      acc[nt][0] += s0 * g[nt][0] + z0 * xs[nt][0];
+      acc[nt][1] += s0 * g[nt][1] + z0 * xs[nt][1];
+      acc[nt][2] += s1 * g[nt][2] + z1 * xs[nt][2];
+      acc[nt][3] += s1 * g[nt][3] + z1 * xs[nt][3];
+    }
+  };
   auto compute = [&](int t, int j, int b) {
     const uint8_t* slot = ring + (t % kR) * kSlot;
     const int rb = rb_of(j);
     const int b0 = s_beg + b * kU;
+    if (b0 + kU <= s_end) {
+      // full batch: every step gets its own accumulators, so the kU steps' MMA chains
+      // are independent
+      float ag[kU][NT][4], ax[kU][NT][4];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int st = b0 + u;
+        const uint4 q = *reinterpret_cast<const uint4*>(slot + u * 512 + lane * 16);
+        uint4 xa[NT], xb[NT];
+        x_frag(st * 64, xa, xb);
+        uint32_t f[4][4];
+        decode(rb, st, q, f);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) ag[u][nt][e] = ax[u][nt][e] = 0.f;
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            uint32_t b0_, b1_;
+            bsel(xa[nt], xb[nt], jj, b0_, b1_);
+            if constexpr (FOLD) mma16816<T>(ax[u][nt], ones, b0_, b1_);
+            mma16816<T>(ag[u][nt], f[jj], b0_, b1_);
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < kSP; ++i) {
+        float g[NT][4], xs[NT][4];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            g[nt][e] = ag[i * G][nt][e];
+            xs[nt][e] = ax[i * G][nt][e];
+#pragma unroll
+            for (int u = 1; u < G; ++u) {
+              g[nt][e] += ag[i * G + u][nt][e];
+              xs[nt][e] += ax[i * G + u][nt][e];
+            }
+          }
+        if constexpr (FOLD) {
+          fold(reinterpret_cast<const float2*>(slot + kU * 512 + i * 128), g, xs);
+        } else {
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[nt][e] += g[nt][e];
+        }
+      }
+      return;
+    }
+    // partial batch (end of a warp's range): one step at a time
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int st = b0 + u;
@@ -328,6 +424,7 @@ gemv_kernel(const GemvArgs a) {
   // after the wait.
   pdl_launch_dependents();
   pdl_wait();
+  if (a.dbg == 2) return;  // tuning only: launch + PDL overhead
   __syncthreads();  // barrier init visible
   auto issue_weak = [&](int j) {
     if (nwt > 0 && j < nrbc) {
@@ -483,6 +580,7 @@ int gemv(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ld
   a.n_rb = L->oc_pad / 16;
   a.rbb = rowblock_bytes(L->bits, L->m_pad);
   a.nsq = L->m_pad / 64;
+  a.dbg = env_int("QEFT_GEMV_DEBUG", 0);
   int gt = (L->g % 64) == 0 ? L->g / 64 : 0;
   if (gt != 1 && gt != 2 && gt != 4) gt = 0;  // generic per-element dequant
   // warps split the quantized steps in whole groups (and whole 3-bit tiles)
