@@ -107,6 +107,12 @@ int qeft_gemm_dgrad(const qeft_linear_t* layer, const void* dy, int64_t lddy, vo
 int qeft_gemm_wgrad(const qeft_linear_t* layer, const void* dy, int64_t lddy, const void* x,
                     int64_t ldx, float* dw, int T, int accumulate, void* workspace,
                     size_t workspace_bytes, void* stream);
+/* wgrad from the saved weak slice only: x_weak[t][j] = x[t][weak_j] (T x k, row pitch
+ * ldxw >= k, ldxw % 8 == 0, 16-byte aligned) -- the TrainableLayerState.x_weak of
+ * qlinear_forward_train (tuning.py:30-34, 70-71), so the forward pass keeps k of IC columns. */
+int qeft_gemm_wgrad_weak(const qeft_linear_t* layer, const void* dy, int64_t lddy, const void* x_weak,
+                         int64_t ldxw, float* dw, int T, int accumulate, void* workspace,
+                         size_t workspace_bytes, void* stream);
 
 /* ---- optimizer (tuning.py:137-160 adam_step, tuning.py:226-236 clip) ---- */
 /* out[0] = sum(g^2) in fp64 (deterministic two-pass). scratch >= 4096 doubles. */

@@ -53,6 +53,7 @@ SIGNATURES = {
     "qeft_gemm_fwd": (_I, [_LP, _VP, _I64, _VP, _I64, _I, _VP, _SZ, _VP]),
     "qeft_gemm_dgrad": (_I, [_LP, _VP, _I64, _VP, _I64, _I, _I, _VP, _SZ, _VP]),
     "qeft_gemm_wgrad": (_I, [_LP, _VP, _I64, _VP, _I64, _VP, _I, _I, _VP, _SZ, _VP]),
+    "qeft_gemm_wgrad_weak": (_I, [_LP, _VP, _I64, _VP, _I64, _VP, _I, _I, _VP, _SZ, _VP]),
     "qeft_grad_sqnorm": (_I, [_VP, _I64, _VP, _VP, _VP]),
     "qeft_div_scalar": (_I, [_VP, _I64, _F, _VP]),
     "qeft_adam_clip": (_I, [_VP, _VP, _VP, _VP, _I64, _VP, _F, _F, _F, _F, _F, _F, _F, _F, _F, _VP, _VP]),

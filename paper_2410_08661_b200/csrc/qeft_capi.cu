@@ -108,6 +108,12 @@ int qeft_gemm_wgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, const 
   return gemm_wgrad(L, dy, lddy, x, ldx, dw, T, acc, ws, wsb, ST(s));
 }
 
+int qeft_gemm_wgrad_weak(const qeft_linear_t* L, const void* dy, int64_t lddy, const void* xw,
+                         int64_t ldxw, float* dw, int T, int acc, void* ws, size_t wsb, void* s) {
+  if (int r = check_layer(L)) return r;
+  return gemm_wgrad(L, dy, lddy, xw, ldxw, dw, T, acc, ws, wsb, ST(s), true);
+}
+
 int qeft_grad_sqnorm(const float* g, int64_t n, double* scratch, double* out, void* s) {
   return grad_sqnorm(g, n, scratch, out, ST(s));
 }

@@ -530,6 +530,14 @@ int make_map(CUtensorMap* m, const void* base, int dtype, int64_t inner, int64_t
   QEFT_CHECK(fn != nullptr, QEFT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   QEFT_CHECK(((uintptr_t)base & 15) == 0 && (ld_elems * 2) % 16 == 0, QEFT_ERR_LAYOUT,
              "TMA needs 16-byte aligned base and row stride");
+  // driver-API call: threads that have only used the runtime implicitly (e.g. the
+  // autograd engine's worker) may have no current context yet
+  CUcontext ctx = nullptr;
+  if (cuCtxGetCurrent(&ctx) != CUDA_SUCCESS || ctx == nullptr) {
+    int dev = 0;
+    QEFT_CUDA(cudaGetDevice(&dev));
+    QEFT_CUDA(cudaSetDevice(dev));
+  }
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ld_elems * 2)};
   cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
@@ -685,7 +693,7 @@ int launch_wgrad(const CUtensorMap& md, const CUtensorMap& mx, float* dw, int oc
 }
 
 int gemm_wgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, const void* x, int64_t ldx, float* dw,
-               int T_, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st) {
+               int T_, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st, bool x_is_weak) {
   QEFT_CHECK(T_ >= 1, QEFT_ERR_SHAPE, "gemm_wgrad: T=%d", T_);
   if (L->k == 0) return 0;
   QEFT_CHECK(L->k_pad <= 256, QEFT_ERR_LAYOUT, "gemm_wgrad: k_pad=%d > 256", L->k_pad);
@@ -697,7 +705,12 @@ int gemm_wgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, const void*
   if (int r = pitch_dy(L, dy, lddy, T_, ws_dy, ws_dy_bytes, st)) return r;
   if (int r = make_map(&md, dy, L->act_dtype, L->oc, T_, lddy, 64)) return r;
   const bool fast = (L->flags & QEFT_FLAG_STRUCTURED_FAST) && ldx % 8 == 0 && ((uintptr_t)x & 15) == 0;
-  if (fast) {
+  if (x_is_weak) {
+    // the caller saved only x[:, weak] (T x k, row pitch ldx) in the forward pass
+    QEFT_CHECK(ldx >= L->k && ldx % 8 == 0 && ((uintptr_t)x & 15) == 0, QEFT_ERR_SHAPE,
+               "gemm_wgrad_weak: x_weak needs a 16-byte aligned row pitch >= k (ld=%lld)", (long long)ldx);
+    if (int r = make_map(&mx, x, L->act_dtype, L->k, T_, ldx, 64)) return r;
+  } else if (fast) {
     if (int r = make_map(&mx, (const char*)x + (size_t)L->m * 2, L->act_dtype, L->k, T_, ldx, 64)) return r;
   } else {
     QEFT_CHECK(ws_bytes >= xw_bytes, QEFT_ERR_SHAPE, "gemm_wgrad: workspace too small");

@@ -51,7 +51,8 @@ int gemm_fwd(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_
 int gemm_dgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, void* dx, int64_t lddx, int T,
                int accumulate, void* ws, size_t ws_bytes, cudaStream_t st);
 int gemm_wgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, const void* x, int64_t ldx,
-               float* dw, int T, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st);
+               float* dw, int T, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st,
+               bool x_is_weak = false);
 
 int grad_sqnorm(const float* g, int64_t n, double* scratch, double* out, cudaStream_t st);
 int div_scalar(float* g, int64_t n, float d, cudaStream_t st);

@@ -205,6 +205,40 @@ class DeviceLayer:
                                      _lib.stream_ptr()), "gemm_dgrad")
         return out
 
+    def gather_weak(self, x, out=None):
+        """x_weak[t][j] = x[t][weak_j] (T x roundup(k, 8), zero padded): the only slice of the
+        input the weak-column backward needs (TrainableLayerState.x_weak, tuning.py:30-34)."""
+        import torch
+        kw = _pad(self.k, 8)
+        if x.stride(1) != 1:
+            x = x.contiguous()
+        T = x.shape[0]
+        if out is None:
+            out = torch.empty((T, kw), dtype=x.dtype, device=x.device)
+        if self.k:
+            _lib.check(_lib.lib().qeft_gather_cols(
+                _lib.ptr(x), x.stride(0), self.colmap.data_ptr() + 4 * self.m_pad, kw, T,
+                _DT[self.dtype], _lib.ptr(out), _lib.stream_ptr()), "gather_weak")
+        return out
+
+    def gemm_wgrad_weak(self, dy, x_weak, out=None, accumulate=False):
+        """dW_weak[o][j] (+)= sum_t dy[t][o] x_weak[t][j], fp32 (oc, k) from the saved slice."""
+        import torch
+        if dy.stride(1) != 1:
+            dy = dy.contiguous()
+        T = dy.shape[0]
+        if out is None:
+            out = torch.empty((self.oc, self.k), dtype=torch.float32, device=dy.device)
+            accumulate = False
+        if not self.k:
+            return out
+        L = _lib.lib()
+        ws = WORKSPACE.get(int(L.qeft_gemm_workspace_bytes(self.cptr, T)), dy.device)
+        _lib.check(L.qeft_gemm_wgrad_weak(self.cptr, _lib.ptr(dy), dy.stride(0), _lib.ptr(x_weak),
+                                          x_weak.stride(0), _lib.ptr(out), T, int(accumulate),
+                                          _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "gemm_wgrad_weak")
+        return out
+
     def gemm_wgrad(self, dy, x, out=None, accumulate=False):
         """dW_weak[o][j] = sum_t dy[t][o] x[t][weak_j], fp32 (oc, k)."""
         import torch

@@ -1,0 +1,105 @@
+"""QEFTLinear: the structured mixed-precision linear layer as a torch module.
+
+Forward is y = x W_hat^T with W_hat = [dequant(codes) | W_weak] in the layer's
+own column order (quantizer.py:95-100); backward gives dX through the full
+W_hat and dW only for the weak block, computed from the saved weak slice of
+the input (the reference's qlinear_forward_train / qlinear_backward,
+pkg/src/qeft/tuning.py:52-103). Every product runs in libqeft_b200:
+  T <= 16 tokens  -> decode GEMV (qeft_gemv)
+  T  > 16 tokens  -> tcgen05 GEMM (qeft_gemm_fwd)
+  backward        -> qeft_gemm_dgrad + qeft_gemm_wgrad_weak
+The fp32 master of the weak block is the module's only Parameter; its .grad is
+a view into the owner's flat gradient bucket when one is attached (the DP step
+all-reduces that bucket in one call), and the fp16/bf16 kernel copy (weak16)
+is refreshed from the master after each optimizer step.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .errors import ShapeError
+from .layer import DeviceLayer, _DT
+
+
+class _QEFTLinearFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x2, weak32, mod):
+        dl: DeviceLayer = mod.dl
+        T = x2.shape[0]
+        if T <= 16:
+            y = dl.gemv(x2)
+        else:
+            y = dl.gemm_fwd(x2)
+        ctx.mod = mod
+        if weak32.requires_grad and dl.k:
+            ctx.save_for_backward(dl.gather_weak(x2))
+        else:
+            ctx.save_for_backward(None)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        mod = ctx.mod
+        dl: DeviceLayer = mod.dl
+        (xw,) = ctx.saved_tensors
+        dy = dy.contiguous()
+        if dy.dtype != dl.tdtype:
+            dy = dy.to(dl.tdtype)
+        dx = dl.gemm_dgrad(dy) if ctx.needs_input_grad[0] else None
+        if xw is not None:
+            w = mod.weak32
+            if w.grad is None:
+                w.grad = torch.zeros_like(w)
+            # accumulate straight into the (bucket-backed) .grad: micro-batches add up
+            # exactly like the reference's acc[name] += grads[name] (tuning.py:219-224)
+            dl.gemm_wgrad_weak(dy, xw, out=w.grad, accumulate=True)
+        return dx, None, None
+
+
+class QEFTLinear(torch.nn.Module):
+    """A QuantizedLinear (or synthetic B200-layout layer) as an nn.Module."""
+
+    def __init__(self, dl: DeviceLayer, name: str = "", trainable: bool = True):
+        super().__init__()
+        self.dl = dl
+        self.name = name
+        self.oc, self.ic, self.k = dl.oc, dl.ic, dl.k
+        w = dl.weak32
+        if w is None:
+            # synthetic layers carry only the kernel copy; the master is read back from it
+            w = dl.dequant_full()[:, _weak_columns(dl)].contiguous()
+        self.weak32 = torch.nn.Parameter(w.reshape(dl.oc, dl.k).float(), requires_grad=trainable)
+
+    @classmethod
+    def from_quantized(cls, q, dtype="bf16", name="", trainable=True):
+        return cls(DeviceLayer.from_quantized(q, dtype=dtype), name=name, trainable=trainable)
+
+    def forward(self, x):
+        if x.shape[-1] != self.ic:
+            raise ShapeError(f"{self.name}: input width {x.shape[-1]} != IC {self.ic}")
+        lead = x.shape[:-1]
+        x2 = x.reshape(-1, self.ic)
+        if x2.dtype != self.dl.tdtype:
+            x2 = x2.to(self.dl.tdtype)
+        y = _QEFTLinearFn.apply(x2, self.weak32, self)
+        return y.reshape(*lead, self.oc)
+
+    @torch.no_grad()
+    def refresh(self):
+        """Re-pack the kernel's weak16 from the fp32 master (after an update)."""
+        if self.k:
+            _lib.check(_lib.lib().qeft_pack_weak(self.weak32.data_ptr(), self.oc, self.k,
+                                                 _DT[self.dl.dtype], self.dl.weak16.data_ptr(),
+                                                 _lib.stream_ptr()), "pack_weak")
+
+    def extra_repr(self):
+        return (f"oc={self.oc}, ic={self.ic}, k={self.k}, bits={self.dl.bits}, g={self.dl.g}, "
+                f"dtype={self.dl.dtype}")
+
+
+def _weak_columns(dl: DeviceLayer):
+    """Input columns of the weak block, from the colmap (B200 K order -> column)."""
+    cm = dl.colmap[dl.m_pad:dl.m_pad + dl.k].long()
+    return cm

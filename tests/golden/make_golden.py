@@ -208,11 +208,67 @@ def gen_selection():
     np.savez_compressed(os.path.join(OUT, "selection.npz"), **d)
 
 
+def gen_finetune():
+    """Whole-model weak-column fine-tuning on a toy model (reference SMALL_CONFIG shape,
+    pkg/tests/conftest.py:23-24): one forward/backward through the reference engine with
+    QuantLinearTrainOp (loss, logits, every layer's dW_weak) and a 3-step finetune log and
+    final weak blocks, for reorder modes ogr (structured + irregular wo) and online."""
+    from qeft import model as M
+    from qeft import qmodel as Q
+    d = {}
+    cfg = M.ModelConfig(d_model=32, n_heads=4, head_dim=8, d_ff=64, n_blocks=2,
+                        vocab_size=256, max_seq=64, seed=5)
+    dense = M.init_model(cfg)
+    ids = np.random.default_rng(77).integers(0, 256, size=4000).astype(np.int64)
+    hess = calibration.collect_calibration(dense, ids, n_seq=4, seq_len=48, seed=0)
+    d["cfg"] = np.array([cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.d_ff, cfg.n_blocks,
+                         cfg.vocab_size, cfg.max_seq, cfg.seed])
+    d["ids"] = ids
+    for mi, reo in enumerate(("ogr", "online")):
+        qm = Q.quantize_model(dense, hess, k=4, bits=4, g=16, mode="rtn", reorder=reo)
+        pre = f"m{mi}_"
+        d[pre + "embedding"] = qm.embedding
+        d[pre + "final_gain"] = qm.final_gain
+        d[pre + "head"] = qm.head
+        for i, b in enumerate(qm.blocks):
+            d[pre + f"b{i}_gain1"] = b.gain1
+            d[pre + f"b{i}_gain2"] = b.gain2
+        for name, q in qm.layer_items():
+            _layer_dict(pre + name + "_", q, d)
+            d[pre + name + "_input_perm"] = (q.input_perm if q.input_perm is not None
+                                            else np.zeros(0, np.int64))
+        # one traced forward/backward of the engine with the training op
+        rng = np.random.default_rng(11)
+        xb, yb = M.sample_windows(rng, ids, 2, 32)
+        em = Q.quant_engine(qm, op_factory=lambda nm, q: tuning.QuantLinearTrainOp(nm, q))
+        logits, _, cache = M.forward_batch(em, xb, want_cache=True)
+        loss, dlogits = M.cross_entropy_with_grad(logits, yb)
+        grads = M.backward_batch(em, cache, dlogits, param_grads=False)
+        d[pre + "xb"], d[pre + "yb"] = xb, yb
+        d[pre + "logits"] = logits
+        d[pre + "loss"] = loss
+        for name in grads:
+            d[pre + "grad_" + name] = grads[name]
+        # short fine-tune
+        tc = tuning.TuneConfig(steps=3, lr=1e-3, batch=2, grad_accum=2, seq_len=32, seed=2,
+                               log_every=1)
+        tuned, log = tuning.finetune(qm, ids, tc)
+        d[pre + "log_loss"] = np.array([r["loss"] for r in log])
+        d[pre + "log_gnorm"] = np.array([r["grad_norm"] for r in log])
+        d[pre + "log_counts"] = np.array([[r["wgrad_fma"], r["full_fma"], r["saved_elems"],
+                                           r["full_elems"]] for r in log])
+        for name, q in tuned.layer_items():
+            d[pre + "tuned_" + name] = q.weak
+    d["n_models"] = 2
+    np.savez_compressed(os.path.join(OUT, "finetune.npz"), **d)
+
+
 if __name__ == "__main__":
-    gen_packing()
-    gen_quantizer()
-    gen_training()
-    gen_selection()
+    # `make_golden.py [packing quantizer training selection finetune]` (default: all)
+    gens = {"packing": gen_packing, "quantizer": gen_quantizer, "training": gen_training,
+            "selection": gen_selection, "finetune": gen_finetune}
+    for name in (sys.argv[1:] or list(gens)):
+        gens[name]()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))
