@@ -532,8 +532,16 @@ int make_map(CUtensorMap* m, const void* base, int dtype, int64_t inner, int64_t
              "TMA needs 16-byte aligned base and row stride");
   // driver-API call: threads that have only used the runtime implicitly (e.g. the
   // autograd engine's worker) may have no current context yet
+  static auto get_ctx = []() -> CUresult (*)(CUcontext*) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuCtxGetCurrent", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      return (CUresult(*)(CUcontext*))p;
+    return nullptr;
+  }();
   CUcontext ctx = nullptr;
-  if (cuCtxGetCurrent(&ctx) != CUDA_SUCCESS || ctx == nullptr) {
+  if (get_ctx == nullptr || get_ctx(&ctx) != CUDA_SUCCESS || ctx == nullptr) {
     int dev = 0;
     QEFT_CUDA(cudaGetDevice(&dev));
     QEFT_CUDA(cudaSetDevice(dev));
