@@ -269,14 +269,17 @@ def run_b200(args):
     roof = kernel_roofline(torch, min(args.blocks, 32), peak, n) if rank == 0 else []
     n_layers = len(layers)
     del stack, layers
+    torch.cuda.empty_cache()
+    ft = None if args.no_ft else finetune_bench(args, ws, rank, local, torch)
     line = None
     if rank == 0:
-        dom = max(roof, key=lambda r: r["us_per_launch"] * (3 if r["shape"] == [4096, 4096] else 2))
+        count = {(4096, 4096): 4, (11008, 4096): 2, (4096, 11008): 1}
+        dom = max(roof, key=lambda r: r["us_per_launch"] * count[tuple(r["shape"])])
         traffic = None
-        tp = os.path.join(ROOT, "profiles", "gemv_traffic.json")
-        if os.path.exists(tp):
-            tj = json.load(open(tp))
-            traffic = tj.get("%dx%d" % tuple(dom["shape"]))
+        import glob
+        tps = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "gemv_traffic.json")))
+        if tps:  # dram__bytes_read + write per launch from the latest committed ncu capture
+            traffic = json.load(open(tps[-1])).get("%dx%d" % tuple(dom["shape"]))
         cpu = None
         if ws == 1 and not args.no_cpu:
             gbs, sample, cores = cpu_oracle_sample(seconds=args.cpu_seconds)
@@ -293,13 +296,14 @@ def run_b200(args):
             "frac_of_peak": value / ws / peak, "peak_gbs": peak, "peak_kind": peak_kind,
             "roofline": {"bound": "hbm", "achieved": dom["achieved_gbs"], "peak": peak,
                          "unit": "GB/s", "frac": dom["frac"], "traffic": traffic,
-                         "kernel": "qeft gemv_kernel<4,1,half,FOLD> %dx%d" % tuple(dom["shape"]),
+                         "kernel": "gemv_kernel<4-bit, N=1, g=128, fp16> %dx%d (largest share of the step)" % tuple(dom["shape"]),
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                          "per_shape": roof},
             "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": n_layers * args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "finetune": ft,
         }
         line["e2e"]["h2d_bytes_per_step"] = sum(2 * n * ic for ic in sorted({s[1] for s in BLOCK_SHAPES}))
         line["e2e"]["d2h_bytes_per_step"] = sum(2 * n * oc for oc, _ in BLOCK_SHAPES) * args.blocks
@@ -307,6 +311,136 @@ def run_b200(args):
     if ws > 1:
         torch.distributed.destroy_process_group()
     return line
+
+
+def finetune_bench(args, ws, rank, local, torch):
+    """LLaMA-2-7B-shaped QEFT fine-tuning step (BASELINE.json configs[2]): seq 2048,
+    micro-batch args.ft_mb per GPU, data parallel over the ranks with ONE NCCL all-reduce
+    of the flat fp32 weak-gradient bucket per step (174,063,616 params at k=128), then the
+    fused clip + Adam kernels. Synthetic random-init weights in the B200 layout, bf16
+    activations, synthetic tokens. value = tokens/s of the whole job (device-timed, max
+    over ranks); e2e adds the per-step H2D token copy (pinned) and D2H loss read."""
+    import numpy as np
+    import torch.distributed as dist
+    from paper_2410_08661_b200 import _lib
+    from paper_2410_08661_b200.model import QEFTDecoder, cross_entropy_mean
+    from paper_2410_08661_b200.qmodel import LLAMA2_7B, ModelConfig
+    from paper_2410_08661_b200.tuning import TuneConfig, WeakTrainer, dp_allreduce_
+    cfg = ModelConfig(**{**LLAMA2_7B.__dict__, "n_blocks": args.ft_blocks})
+    model = QEFTDecoder.synthetic(cfg, k=128, bits=4, g=128, act_dtype="bf16", compute_dtype="bf16", seed=0)
+    group = dist.group.WORLD if ws > 1 else None
+    tr = WeakTrainer(model, TuneConfig(lr=5e-6, max_grad_norm=0.3), group=group)
+    mb, seq, V = args.ft_mb, args.ft_seq, cfg.vocab_size
+    nsteps = args.ft_warmup + args.ft_steps
+    rng = np.random.default_rng(1000 + rank)  # disjoint synthetic micro-batches per rank
+    host = torch.from_numpy(rng.integers(0, V, size=(nsteps, mb, seq + 1))).pin_memory()
+    dev = torch.empty((mb, seq + 1), dtype=torch.int64, device="cuda")
+    loss_host = torch.empty((), dtype=torch.float64).pin_memory()
+
+    def step(i, e2e=False):
+        if e2e:
+            dev.copy_(host[i], non_blocking=True)
+        tr.zero_grad()
+        loss = cross_entropy_mean(model(dev[:, :-1]), dev[:, 1:])
+        loss.backward()
+        loss_sum = loss.detach().double()
+        dp_allreduce_(tr.grad, loss_sum, group)
+        tr.step(ws, reduced=True)
+        if e2e:
+            loss_host.copy_(loss_sum)  # D2H read of the step's loss (synchronizes)
+
+    dev.copy_(host[0])
+    for i in range(args.ft_warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    calls0 = _lib.CALLS[0]
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(args.ft_steps):
+            step(i)
+        e1.record()
+        torch.cuda.synchronize()
+    calls = (_lib.CALLS[0] - calls0) // args.ft_steps
+    t = e0.elapsed_time(e1) / 1e3 / args.ft_steps
+    if ws > 1:
+        tt = torch.tensor([t], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+        dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(args.ft_steps):
+        step(args.ft_warmup + i if args.ft_warmup + i < nsteps else i, e2e=True)
+    te = (time.perf_counter() - t0) / args.ft_steps
+    if ws > 1:
+        tt = torch.tensor([te], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        te = float(tt.item())
+    tokens = ws * mb * seq
+    flops_tok = 28.39e9 * args.ft_blocks / 32  # SURVEY.md 8(d): 7B linears+attention+head per token
+    tf_peak = _bf16_peak()
+    gemm = gemm_roofline(torch, seq) if rank == 0 else None
+    del model, tr
+    torch.cuda.empty_cache()
+    return {"metric": "QEFT fine-tune tokens/s", "value": tokens / t, "unit": "tokens/s",
+            "ms_per_step": t * 1e3, "steps": args.ft_steps, "warmup": args.ft_warmup,
+            "config": {"workload": "LLaMA-2-7B-shaped QEFT fine-tuning step (4-bit g128 k=128, "
+                                   f"{args.ft_blocks} blocks), seq {seq}, micro-batch {mb}/GPU",
+                       "global_batch_tokens": tokens, "parallelism": f"dp{ws}",
+                       "weak_params": tr_params(cfg), "allreduce_bytes": 4 * tr_params(cfg),
+                       "l2": "activations and weights far above L2"},
+            "dtype": "bf16", "scaling": "weak", "data": "synthetic",
+            "mfu": tokens / t * flops_tok / (ws * tf_peak * 1e12), "tflops_peak": tf_peak,
+            "e2e": {"value": tokens / te, "unit": "tokens/s", "h2d_bytes_per_step": mb * (seq + 1) * 8,
+                    "d2h_bytes_per_step": 8},
+            "gpu_launches": calls * args.ft_steps, "gpu_launches_note": "libqeft_b200 C-ABI calls in the timed region (each launches 1-2 kernels)",
+            "roofline": gemm, "clocks": clk.summary()}
+
+
+def tr_params(cfg, k=128):
+    """Weak-block parameters: k columns x output channels of every block linear."""
+    return cfg.n_blocks * k * (4 * cfg.d_model + 2 * cfg.d_ff + cfg.d_model)
+
+
+def _bf16_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("bf16_tflops_sustained", d["bf16_tflops"]))
+    return 1400.0
+
+
+def gemm_roofline(torch, T):
+    """Dominant kernel of the step: the tcgen05 forward GEMM (dequant producer + TMA
+    activations), timed alone on the 7B shapes at T tokens with CUDA events."""
+    from paper_2410_08661_b200.decode import random_layer
+    peak = _bf16_peak()
+    out = []
+    for oc, ic in ((4096, 4096), (11008, 4096), (4096, 11008)):
+        dl = random_layer(oc, ic, 128, 4, 128, "bf16", seed=5)
+        x = torch.randn(T, ic, device="cuda", dtype=torch.bfloat16)
+        y = torch.empty(T, oc, device="cuda", dtype=torch.bfloat16)
+        for _ in range(3):
+            dl.gemm_fwd(x, out=y)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 20
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            dl.gemm_fwd(x, out=y)
+        e1.record()
+        torch.cuda.synchronize()
+        s = e0.elapsed_time(e1) / 1e3 / reps
+        fl = 2.0 * T * oc * ic
+        out.append({"shape": [oc, ic], "T": T, "us": s * 1e6, "tflops": fl / s / 1e12,
+                    "frac": fl / s / 1e12 / peak})
+    dom = max(out, key=lambda r: r["us"] * (2 if r["shape"] == [11008, 4096] else 1))
+    return {"bound": "tensor", "achieved": dom["tflops"], "peak": peak, "unit": "TFLOP/s",
+            "frac": dom["frac"], "traffic": None,
+            "kernel": "gemm_kernel<fwd, 4-bit, bf16> %dx%d T=%d" % (dom["shape"][0], dom["shape"][1], T),
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained", "per_shape": out}
 
 
 def main():
@@ -319,6 +453,12 @@ def main():
     ap.add_argument("--blocks", type=int, default=32)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ft", action="store_true", help="skip the fine-tune step measurement")
+    ap.add_argument("--ft-blocks", type=int, default=32)
+    ap.add_argument("--ft-seq", type=int, default=2048)
+    ap.add_argument("--ft-mb", type=int, default=1)
+    ap.add_argument("--ft-steps", type=int, default=5)
+    ap.add_argument("--ft-warmup", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

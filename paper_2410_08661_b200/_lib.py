@@ -90,7 +90,11 @@ def lib():
     return _lib
 
 
+CALLS = [0]  # C-ABI calls made through check() (bench.py reports them per timed region)
+
+
 def check(rc: int, what: str) -> None:
+    CALLS[0] += 1
     if rc == 0:
         return
     msg = lib().qeft_last_error().decode(errors="replace")

@@ -420,7 +420,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
 template <typename T, int NW>
 __global__ void __launch_bounds__(192, 1)
 wgrad_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_constant__ CUtensorMap map_xw,
-             float* __restrict__ dw, int oc, int k, int T_, int accumulate) {
+             float* __restrict__ dw, int oc, int k, int T_, int accumulate, int kb_split) {
+  // split-K over tokens: blockIdx.y takes k-blocks [y * kb_split, (y + 1) * kb_split); with
+  // gridDim.y > 1 each split stores its fp32 partial at dw + y * oc * k (a workspace) and
+  // wgrad_reduce_kernel sums the splits in order (deterministic).
   constexpr int N = NW * 64;
   constexpr int kSA = BM * 64 * 2;         // 16 KB: 2 boxes of 64 channels x 64 tokens
   constexpr int kSB = N * 64 * 2;          // NW boxes of 64 weak columns x 64 tokens
@@ -434,7 +437,12 @@ wgrad_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_constant__
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int o0 = blockIdx.x * BM;
-  const int nkb = (T_ + 63) / 64;
+  const int kb0 = blockIdx.y * kb_split;
+  const int nkb = min((T_ + 63) / 64 - kb0, kb_split);
+  if (gridDim.y > 1) {
+    dw += (int64_t)blockIdx.y * oc * k;
+    accumulate = 0;
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -456,10 +464,11 @@ wgrad_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_constant__
         const int s = kb % kStages;
         mbar_wait(&empty_bar[s], ((kb / kStages) & 1) ^ 1);
         mbar_expect_tx(&full_bar[s], kSA + kSB);
-        tc::tma_load_2d(sA + s * kSA, &map_dy, o0, kb * 64, &full_bar[s]);
-        tc::tma_load_2d(sA + s * kSA + 8192, &map_dy, o0 + 64, kb * 64, &full_bar[s]);
+        const int t0 = (kb0 + kb) * 64;
+        tc::tma_load_2d(sA + s * kSA, &map_dy, o0, t0, &full_bar[s]);
+        tc::tma_load_2d(sA + s * kSA + 8192, &map_dy, o0 + 64, t0, &full_bar[s]);
 #pragma unroll
-        for (int b = 0; b < NW; ++b) tc::tma_load_2d(sB + s * kSB + b * 8192, &map_xw, b * 64, kb * 64, &full_bar[s]);
+        for (int b = 0; b < NW; ++b) tc::tma_load_2d(sB + s * kSB + b * 8192, &map_xw, b * 64, t0, &full_bar[s]);
       }
     }
   } else if (warp == 1) {
@@ -505,6 +514,18 @@ wgrad_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_constant__
   if (warp == 1) {
     tc::fence_after();
     tc::tmem_dealloc(tmem, kCols);
+  }
+}
+
+// dw[i] (+)= sum_s part[s][i], s = 0..splits-1 in order (deterministic split-K reduction)
+__global__ void wgrad_reduce_kernel(const float* __restrict__ part, float* __restrict__ dw, int64_t n,
+                                    int splits, int accumulate) {
+  pdl_launch_dependents();
+  pdl_wait();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float v = accumulate ? dw[i] : 0.f;
+    for (int s = 0; s < splits; ++s) v += part[(int64_t)s * n + i];
+    dw[i] = v;
   }
 }
 
@@ -613,11 +634,20 @@ GemmArgs base_args(const qeft_linear_t* L, int T_) {
 
 namespace qeft {
 
+// split count for the wgrad token reduction: fill ~2 CTAs per SM, >= 4 k-blocks per split
+int wgrad_splits(int oc, int T_) {
+  const int mb = (oc + BM - 1) / BM, nkb = (T_ + 63) / 64;
+  int s = (2 * num_sms() + mb - 1) / mb;
+  s = std::min(s, std::max(1, nkb / 4));
+  return std::max(1, std::min(s, 16));
+}
+
 size_t gemm_workspace_bytes(const qeft_linear_t* L, int T_) {
   // gathered activations in B200 K order (fwd, non-structured layouts), weak columns
   // (wgrad), or a 16-byte-pitched copy of dY (dgrad/wgrad when oc % 8 != 0)
   const size_t kk = (size_t)std::max(L->m_pad + L->k_pad, pad_to(L->oc, 8) + L->k_pad);
-  return (size_t)T_ * kk * 2 + 1024;
+  const size_t part = L->k ? (size_t)wgrad_splits(L->oc, T_) * L->oc * L->k * 4 + 256 : 0;
+  return (size_t)T_ * kk * 2 + part + 1024;
 }
 
 // dY with a row pitch TMA cannot address -> copy into ws with pitch roundup(oc, 8)
@@ -687,7 +717,7 @@ int gemm_dgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, void* dx, i
 
 template <typename T, int NW>
 int launch_wgrad(const CUtensorMap& md, const CUtensorMap& mx, float* dw, int oc, int k, int T_, int acc,
-                 cudaStream_t st) {
+                 float* part, cudaStream_t st) {
   constexpr int kStages = 4;
   const size_t smem = 1024 + (size_t)kStages * (BM * 64 * 2 + NW * 64 * 64 * 2);
   auto kern = wgrad_kernel<T, NW>;
@@ -696,7 +726,19 @@ int launch_wgrad(const CUtensorMap& md, const CUtensorMap& mx, float* dw, int oc
     QEFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  QEFT_CUDA(launch_pdl(kern, dim3((oc + BM - 1) / BM), dim3(192), smem, st, md, mx, dw, oc, k, T_, acc));
+  const int nkb = (T_ + 63) / 64;
+  const int splits = part ? wgrad_splits(oc, T_) : 1;
+  const int kbs = (nkb + splits - 1) / splits;
+  const int ns = (nkb + kbs - 1) / kbs;  // splits actually used
+  float* out = ns > 1 ? part : dw;
+  QEFT_CUDA(launch_pdl(kern, dim3((oc + BM - 1) / BM, ns), dim3(192), smem, st, md, mx, out, oc, k, T_, acc,
+                       kbs));
+  if (ns > 1) {
+    const int64_t n = (int64_t)oc * k;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 4 * num_sms());
+    QEFT_CUDA(launch_pdl(wgrad_reduce_kernel, dim3(blocks), dim3(256), 0, st, (const float*)part, dw, n, ns,
+                         acc));
+  }
   return 0;
 }
 
@@ -706,10 +748,14 @@ int gemm_wgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, const void*
   if (L->k == 0) return 0;
   QEFT_CHECK(L->k_pad <= 256, QEFT_ERR_LAYOUT, "gemm_wgrad: k_pad=%d > 256", L->k_pad);
   CUtensorMap md, mx;
-  // workspace: [weak columns of x (T x k_pad)] [pitched dY copy]
+  // workspace: [weak columns of x (T x k_pad)] [split-K partials] [pitched dY copy]
   const size_t xw_bytes = (size_t)T_ * L->k_pad * 2;
-  void* ws_dy = (char*)ws + ((xw_bytes + 255) & ~(size_t)255);
-  const size_t ws_dy_bytes = ws_bytes > ((xw_bytes + 255) & ~(size_t)255) ? ws_bytes - ((xw_bytes + 255) & ~(size_t)255) : 0;
+  const size_t part_off = (xw_bytes + 255) & ~(size_t)255;
+  const size_t part_bytes = (size_t)wgrad_splits(L->oc, T_) * L->oc * L->k * 4;
+  float* part = ws_bytes >= part_off + part_bytes ? (float*)((char*)ws + part_off) : nullptr;
+  const size_t dy_off = part ? ((part_off + part_bytes + 255) & ~(size_t)255) : part_off;
+  void* ws_dy = (char*)ws + dy_off;
+  const size_t ws_dy_bytes = ws_bytes > dy_off ? ws_bytes - dy_off : 0;
   if (int r = pitch_dy(L, dy, lddy, T_, ws_dy, ws_dy_bytes, st)) return r;
   if (int r = make_map(&md, dy, L->act_dtype, L->oc, T_, lddy, 64)) return r;
   const bool fast = (L->flags & QEFT_FLAG_STRUCTURED_FAST) && ldx % 8 == 0 && ((uintptr_t)x & 15) == 0;
@@ -729,8 +775,8 @@ int gemm_wgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, const void*
   const bool bf = L->act_dtype == QEFT_BF16;
 #define QEFT_WG(NW)                                                                              \
   if (nw == NW)                                                                                  \
-    return bf ? launch_wgrad<__nv_bfloat16, NW>(md, mx, dw, L->oc, L->k, T_, accumulate, st)     \
-              : launch_wgrad<__half, NW>(md, mx, dw, L->oc, L->k, T_, accumulate, st);
+    return bf ? launch_wgrad<__nv_bfloat16, NW>(md, mx, dw, L->oc, L->k, T_, accumulate, part, st) \
+              : launch_wgrad<__half, NW>(md, mx, dw, L->oc, L->k, T_, accumulate, part, st);
   QEFT_WG(1) QEFT_WG(2) QEFT_WG(3) QEFT_WG(4)
 #undef QEFT_WG
   set_error("gemm_wgrad: unsupported k_pad");

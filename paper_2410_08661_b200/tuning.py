@@ -160,6 +160,33 @@ def sample_windows(rng, ids, n, seq_len):
     return w[:, :-1], w[:, 1:]
 
 
+def rank_micro_batches(rng, ids, cfg: TuneConfig, rank: int = 0, world: int = 1):
+    """One optimizer step's micro-batches for `rank` of `world`.
+
+    Every rank draws the full stream of `grad_accum` windows from the shared
+    generator, in the reference's order (tuning.py:209-213), and keeps those with
+    index % world == rank, so the union over ranks is exactly the reference's
+    accumulation group and the generator stays in lockstep across ranks.
+    Returns [(index, inputs, targets), ...].
+    """
+    out = []
+    for i in range(cfg.grad_accum):
+        xb, yb = sample_windows(rng, ids, cfg.batch, cfg.seq_len)
+        if i % world == rank:
+            out.append((i, xb, yb))
+    return out
+
+
+def dp_allreduce_(grad, loss_sum, group=None):
+    """Sum the flat weak-gradient bucket and the loss sum over the DP group
+    (one collective each; a no-op for a single process)."""
+    import torch.distributed as dist
+    if group is not None and dist.get_world_size(group) > 1:
+        dist.all_reduce(grad, group=group)
+        dist.all_reduce(loss_sum, group=group)
+    return grad, loss_sum
+
+
 class WeakTrainer:
     """Flat-bucket weak-column optimizer state for a QEFTDecoder.
 
@@ -201,14 +228,16 @@ class WeakTrainer:
     def zero_grad(self):
         self.grad.zero_()
 
-    def step(self, n_micro_total: int):
-        """All-reduce (DP) -> /(grad_accum * loss_scale) -> clip -> Adam -> weak16 refresh.
-        Returns the pre-clip global gradient norm as a device fp64 tensor."""
-        import torch.distributed as dist
+    def step(self, n_micro_total: int, loss_sum=None, reduced: bool = False):
+        """All-reduce (DP, unless `reduced`) -> /(grad_accum * loss_scale) -> clip -> Adam
+        -> weak16 refresh. Returns the pre-clip global gradient norm (device fp64)."""
+        import torch
         from . import optim
         cfg = self.cfg
-        if self.group is not None and dist.get_world_size(self.group) > 1:
-            dist.all_reduce(self.grad, group=self.group)
+        if not reduced:
+            if loss_sum is None:
+                loss_sum = torch.zeros((), dtype=torch.float64, device=self.grad.device)
+            dp_allreduce_(self.grad, loss_sum, self.group)
         optim.div_(self.grad, float(n_micro_total) * self.loss_scale)
         optim.grad_sqnorm(self.grad, out=self.sq)
         self.step_no += 1
@@ -266,22 +295,19 @@ def finetune(qm, dataset, config: TuneConfig | None = None, *, act_dtype: str = 
     for step in range(1, cfg.steps + 1):
         tr.zero_grad()
         loss_sum = torch.zeros((), dtype=torch.float64, device=dev)
-        for i in range(cfg.grad_accum):
-            xb, yb = sample_windows(rng, ids, cfg.batch, cfg.seq_len)  # every rank draws every batch
-            if i % world != rank:
-                continue
+        for _, xb, yb in rank_micro_batches(rng, ids, cfg, rank, world):
             xt = torch.from_numpy(np.asarray(xb, np.int64)).to(dev)
             yt = torch.from_numpy(np.asarray(yb, np.int64)).to(dev)
             loss = cross_entropy_mean(model(xt), yt)
             (loss * loss_scale).backward()
             loss_sum += loss.detach().double()
-        if world > 1:
-            dist.all_reduce(loss_sum, group=group)
+        dp_allreduce_(tr.grad, loss_sum, group)
         loss_mean = float(loss_sum) / cfg.grad_accum
         if not math.isfinite(loss_mean):
+            # the masters still hold the last finite update (tuning.py:215-218)
             raise DivergenceError(f"non-finite loss at step {step}", last_good=_export(tuned, tr),
                                   step=step)
-        sq = tr.step(cfg.grad_accum)
+        sq = tr.step(cfg.grad_accum, reduced=True)
         if int(tr.flag.item()):
             raise DivergenceError("non-finite gradient in adam_step", last_good=_export(tuned, tr),
                                   step=step)
