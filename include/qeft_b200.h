@@ -87,8 +87,8 @@ int qeft_quantize_rtn(const float* w_dense, int oc, int m, int g, int bits, floa
 
 /* ---- decode GEMV (kernels.py:87-157 matvec_structured/irregular/online) ----
  * y[n][o] = sum_i W_hat[o][i] * x[n][i] for n < n_cols (1..16), x/y row-major.
- * y is act_dtype, or fp32 when y_f32 != 0. Needs qeft_gemv_workspace_bytes()
- * of zero-initialised workspace (kernels leave it zeroed for the next call). */
+ * y is act_dtype, or fp32 when y_f32 != 0. Needs qeft_gemv_workspace_bytes() of
+ * scratch (the x gather buffer of irregular / online-reorder layouts). */
 size_t qeft_gemv_workspace_bytes(const qeft_linear_t* layer, int n_cols);
 int qeft_gemv(const qeft_linear_t* layer, const void* x, int64_t ldx, void* y, int64_t ldy, int y_f32,
               int n_cols, void* workspace, size_t workspace_bytes, void* stream);
