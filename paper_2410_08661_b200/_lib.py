@@ -14,7 +14,7 @@ import subprocess
 from .errors import ShapeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqeft_b200.so")
+LIB_PATH = os.environ.get("QEFT_LIB_PATH") or os.path.join(_HERE, "libqeft_b200.so")  # override: A/B tuning
 CSRC = os.path.join(_HERE, "csrc")
 
 QEFT_F16 = 0

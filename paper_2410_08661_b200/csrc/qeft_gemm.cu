@@ -52,6 +52,7 @@ struct GemmArgs {
   int gathered;   // fwd: B from one map over a gathered B200-order buffer
   int fast_out;   // dgrad: output columns contiguous in 32-blocks (structured, m % 32 == 0)
   int out_cols;   // fwd: oc; dgrad: ic
+  int g_shift;    // log2(g) when g is a power of two, else -1 (group index without a divide)
 };
 
 template <typename T>
@@ -255,7 +256,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
           }
           if (fold16) {
             const float2* szr = a.sz + (int64_t)rb * a.ng * 16;
-            const int gi = min((jt * BK + 16 * t4) / a.g, a.ng - 1);
+            const int col = jt * BK + 16 * t4;
+            const int gi = min(a.g_shift >= 0 ? (col >> a.g_shift) : col / a.g, a.ng - 1);
             P.p0[h] = szr[gi * 16 + g8];
             P.p1[h] = szr[gi * 16 + g8 + 8];
           }
@@ -313,14 +315,28 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
         *reinterpret_cast<uint4*>(st + o3) = make_uint4(out[12], out[13], out[14], out[15]);
       }
     };
-    // flatten (tile, kb) into one stream so the prefetch crosses tile boundaries
+    // flatten (tile, kb) into one stream so the prefetch crosses tile boundaries; the
+    // stream is walked with incremental cursors (no integer divides per k-block)
     const int per = a.n_kblk;
     const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     const int total = my_tiles * per;
-    auto coords = [&](int idx, int& m_blk, int& kb) {
-      const int tile = blockIdx.x + (idx / per) * gridDim.x;
-      m_blk = tile % a.n_mblk;
-      kb = idx % per;
+    struct Cursor {
+      int tile, m_blk, kb;
+    };
+    auto advance = [&](Cursor& c) {
+      if (++c.kb == per) {
+        c.kb = 0;
+        c.tile += gridDim.x;
+        c.m_blk += gridDim.x;
+        while (c.m_blk >= a.n_mblk) c.m_blk -= a.n_mblk;
+      }
+    };
+    Cursor cl{(int)blockIdx.x, (int)blockIdx.x % a.n_mblk, 0};  // load cursor (2 ahead)
+    Cursor cp = cl;                                              // process cursor
+    auto coords = [&](int, int& m_blk, int& kb) {  // next position of the load cursor
+      m_blk = cl.m_blk;
+      kb = cl.kb;
+      advance(cl);
     };
     Pre P0, P1, P2;  // register ring, rotated by value (no dynamic indexing -> no local memory)
     if (total > 0) {
@@ -339,8 +355,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
         coords(it + 2, mb, kb);
         load(mb, kb, P2);
       }
-      int mb, kb;
-      coords(it, mb, kb);
+      const int mb = cp.m_blk, kb = cp.kb;
+      advance(cp);
       const int s = it % kStages;
       mbar_wait(&empty_bar[s], ((it / kStages) & 1) ^ 1);
       process(mb, kb, P0, sA + s * kStageA);
@@ -626,6 +642,7 @@ GemmArgs base_args(const qeft_linear_t* L, int T_) {
   a.colmap = L->colmap;
   a.oc = L->oc; a.m = L->m; a.m_pad = L->m_pad; a.k = L->k; a.k_pad = L->k_pad;
   a.g = L->g; a.ng = L->ng;
+  a.g_shift = (L->g & (L->g - 1)) == 0 ? __builtin_ctz((unsigned)L->g) : -1;
   a.T = T_;
   return a;
 }
