@@ -7,7 +7,8 @@
 //   wgrad  dW[o][w] = sum_t dY[t][o] X[t][weak_w]          (qlinear_backward, dW_weak)
 // W_hat is never materialized in HBM: warp-specialized persistent kernels
 //   * dequantize the 3/4-bit tile layout straight into SWIZZLE_128B shared memory
-//     (K-major for fwd, MN-major for dgrad) with 4 producer warps,
+//     (K-major for fwd, MN-major for dgrad) with 8 producer warps (their instruction
+//     rate, not load latency, bounds the tensor pipe: measured),
 //   * stream activations with TMA (cp.async.bulk.tensor, OOB zero fill covers the
 //     quantized/weak split of the B200 K order),
 //   * issue tcgen05.mma (M=128, N=BN, K=16, fp32 accumulators in TMEM, double
@@ -32,7 +33,8 @@ enum { MODE_FWD = 0, MODE_DGRAD = 1 };
 
 constexpr int BM = 128;                 // MMA M (rows of W_hat or of W_hat^T)
 constexpr int BK = 64;                  // K per stage (one SWIZZLE_128B row of fp16)
-constexpr int kProdWarps = 4;           // dequant producers
+constexpr int kProdWarps = 8;           // dequant producers (two per SM sub-partition)
+constexpr int kUPW = 8 / kProdWarps;    // 16x64 A units per producer warp per k-block
 constexpr int kEpiWarps = 4;
 constexpr int kThreads = (2 + kProdWarps + kEpiWarps) * 32;  // TMA, MMA, producers, epilogue
 constexpr int kStageA = BM * BK * 2;    // 16 KB
@@ -218,31 +220,33 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
   } else if (warp < 2 + kProdWarps) {
     // ================= dequant producers: the A operand =================
     // Each warp fills two 16-row x 64-column units of the A tile per k-block:
-    //   fwd:   unit h = row-block 8*m_blk + 2*pw + h, B200 columns 64*kb.. (K-major rows)
-    //   dgrad: unit h = row-block 4*kb + pw, B200 columns 64*(2*m_blk + h).. (MN-major)
+    // Unit u = pw * kUPW + h (0..7) of the 128 x 64 A tile:
+    //   fwd:   row-block 8*m_blk + u, B200 columns 64*kb.. (K-major rows)
+    //   dgrad: row-block 4*kb + u/2, B200 columns 64*(2*m_blk + u%2).. (MN-major)
     // Global loads for k-block kb+2 are issued before k-block kb is processed.
     const int pw = warp - 2;
     const int g8 = lane >> 2, t4 = lane & 3;
     const bool fold16 = (a.g % 16) == 0;
     struct Pre {
-      uint4 v[2][4];   // quant: v[h][0] = lane codes (3-bit: .x,.y = 2-bit words, .z = hi word); weak: 64 B
-      float2 p0[2], p1[2];
+      uint4 v[kUPW][4];   // quant: v[h][0] = lane codes (3-bit: .x,.y = 2-bit words, .z = hi word); weak: 64 B
+      float2 p0[kUPW], p1[kUPW];
     };
     // unit geometry: row-block, 64-column tile index in the B200 order, weak tile (or -1)
     auto unit = [&](int m_blk, int kb, int h, int& rb, int& jt, int& kw) {
+      const int u = pw * kUPW + h;  // A unit 0..7 of the k-block
       if (MODE == MODE_FWD) {
-        rb = m_blk * 8 + 2 * pw + h;
+        rb = m_blk * 8 + u;
         jt = kb;
         kw = kb >= a.kq ? kb - a.kq : -1;
       } else {
-        rb = kb * 4 + pw;
-        jt = 2 * m_blk + h;
-        kw = m_blk >= a.kq ? (m_blk - a.kq) * 2 + h : -1;
+        rb = kb * 4 + (u >> 1);
+        jt = 2 * m_blk + (u & 1);
+        kw = m_blk >= a.kq ? (m_blk - a.kq) * 2 + (u & 1) : -1;
       }
     };
     auto load = [&](int m_blk, int kb, Pre& P) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < kUPW; ++h) {
         int rb, jt, kw;
         unit(m_blk, kb, h, rb, jt, kw);
         if (rb * 16 >= a.oc || (kw >= 0 && kw * 64 >= a.k_pad)) continue;
@@ -272,7 +276,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     };
     auto process = [&](int m_blk, int kb, const Pre& P, uint8_t* st) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < kUPW; ++h) {
         int rb, jt, kw;
         unit(m_blk, kb, h, rb, jt, kw);
         uint32_t out[16];
@@ -297,13 +301,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
         }
         uint32_t o0, o1, o2, o3;  // byte offsets of (row g, chunk 2t), (g, 2t+1), (g+8, 2t), (g+8, 2t+1)
         if (MODE == MODE_FWD) {
-          const int r0 = 16 * (2 * pw + h) + g8, r1 = r0 + 8;
+          const int r0 = 16 * (pw * kUPW + h) + g8, r1 = r0 + 8;
           o0 = tc::sw128(r0, 2 * t4); o1 = tc::sw128(r0, 2 * t4 + 1);
           o2 = tc::sw128(r1, 2 * t4); o3 = tc::sw128(r1, 2 * t4 + 1);
         } else {
           // MN-major: (m, k) at (m/64)*8192 + (k/8)*1024 + sw128(k%8, (m%64)/8)
-          const int kr0 = 16 * pw + g8, kr1 = kr0 + 8;
-          const uint32_t base = h * 8192;
+          const int u = pw * kUPW + h;
+          const int kr0 = 16 * (u >> 1) + g8, kr1 = kr0 + 8;
+          const uint32_t base = (u & 1) * 8192;
           o0 = base + (kr0 >> 3) * 1024 + tc::sw128(kr0 & 7, 2 * t4);
           o1 = base + (kr0 >> 3) * 1024 + tc::sw128(kr0 & 7, 2 * t4 + 1);
           o2 = base + (kr1 >> 3) * 1024 + tc::sw128(kr1 & 7, 2 * t4);
