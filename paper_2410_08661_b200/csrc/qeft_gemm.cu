@@ -95,6 +95,50 @@ QEFT_DEV void dequant_lane(const uint32_t* words, uint32_t hb, float2 p0, float2
   }
 }
 
+// Packed path: the same fragments in the activation dtype's paired arithmetic.
+// (magic + c) - magic = c exactly (HSUB2); c * s rounds once (HFMA2 into the high part of
+// the zero point), then the low part of the zero point is added (HADD2). Splitting
+// z = z_hi + z_lo keeps the per-group offset exact to ~2^-17, so no systematic per-group
+// error appears; the scale carries one rounding to T (<= 2^-9 relative).
+template <int BITS, typename T>
+QEFT_DEV void dequant_lane_packed(const uint32_t* words, uint32_t hb, float2 p0, float2 p1, uint32_t out[16]) {
+  using T2 = typename DTraits<T>::T2;
+  constexpr bool hi = (BITS == 4) && DTraits<T>::kHiTrick;  // fp16 rows g+8 hold magic + 16 c
+  uint32_t mw = DTraits<T>::kMagic;
+  const T2 M2 = *reinterpret_cast<T2*>(&mw);
+  auto split = [](float z, T2& zh, T2& zl) {
+    const T h = from_f32<T>(z);
+    const T l = from_f32<T>(z - to_f32<T>(h));
+    zh.x = zh.y = h;
+    zl.x = zl.y = l;
+  };
+  T2 S0, S1, Z0h, Z0l, Z1h, Z1l;
+  S0.x = S0.y = from_f32<T>(p0.x);
+  S1.x = S1.y = from_f32<T>(hi ? p1.x * (1.f / 16.f) : p1.x);
+  split(p0.y, Z0h, Z0l);
+  split(p1.y, Z1h, Z1l);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t f[4];
+    if constexpr (BITS == 4) {
+      decode4<T>(words[j], f);
+    } else {
+#pragma unroll
+      for (int pp = 0; pp < 4; ++pp) f[pp] = decode3_pair<T>(words[j >> 1], hb, 4 * (j & 1) + pp, j >> 1);
+    }
+    T2 v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const T2 c = __hsub2(*reinterpret_cast<const T2*>(&f[e]), M2);
+      v[e] = (e & 1) ? __hadd2(__hfma2(c, S1, Z1h), Z1l) : __hadd2(__hfma2(c, S0, Z0h), Z0l);
+    }
+    out[2 * j] = *reinterpret_cast<uint32_t*>(&v[0]);          // row g,   cols c, c+1
+    out[2 * j + 1] = *reinterpret_cast<uint32_t*>(&v[2]);      // row g,   cols c+2, c+3
+    out[8 + 2 * j] = *reinterpret_cast<uint32_t*>(&v[1]);      // row g+8, cols c, c+1
+    out[8 + 2 * j + 1] = *reinterpret_cast<uint32_t*>(&v[3]);  // row g+8, cols c+2, c+3
+  }
+}
+
 // general group sizes: per-element (scale, zero)
 template <int BITS, typename T>
 QEFT_DEV void dequant_lane_general(const uint32_t* words, uint32_t hb, const float2* szrow0,
@@ -287,7 +331,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
           const uint32_t words[4] = {P.v[h][0].x, P.v[h][0].y, P.v[h][0].z, P.v[h][0].w};
           const uint32_t hb = (BITS == 3) ? P.v[h][0].z : 0u;
           if (fold16) {
-            dequant_lane<BITS, T>(words, hb, P.p0[h], P.p1[h], out);
+            dequant_lane_packed<BITS, T>(words, hb, P.p0[h], P.p1[h], out);
           } else {
             const float2* szr = a.sz + (int64_t)rb * a.ng * 16;
             dequant_lane_general<BITS, T>(words, hb, szr + g8, szr + g8 + 8, jt * BK + 16 * t4, a.g, a.ng, out);
