@@ -138,6 +138,22 @@ typedef struct qeft_shadow_desc {
 int qeft_weak_shadow(const float* w32, const qeft_shadow_desc_t* descs, int n_layers, int max_elems,
                      void* stream);
 
+/* ---- fused elementwise ops of the fine-tuning host model (model.py:249-275, 389-391) ----
+ * Activations row-major fp16/bf16 (dt), fp32 math; gains frozen (tuning.py: param_grads=False).
+ * rmsnorm: y = gain * x * rstd, rstd[row] = 1/sqrt(mean(x^2) + 1e-5); C % 8 == 0.
+ * rmsnorm_bwd: dx = gain*dy*rstd - x*rstd^3*sum(gain*dy*x)/C (+ dres if non-NULL).
+ * rope: rotate (j, j + hd/2) pairs of every head of rows = B*T tokens (token t = row % T) by
+ *       angle t*inv_freq[j] using cos/sin tables [T][hd/2]; inverse != 0 rotates back (backward).
+ * silu_mul: f = silu(g) * u and (dg, du) from df; n % 8 == 0. */
+int qeft_rmsnorm_fwd(const void* x, const float* gain, void* y, float* rstd, int rows, int C, int dt, void* stream);
+int qeft_rmsnorm_bwd(const void* dy, const void* x, const float* gain, const float* rstd, const void* dres,
+                     void* dx, int rows, int C, int dt, void* stream);
+int qeft_rope(const void* in, void* out, const float* cos_t, const float* sin_t, int64_t rows, int T, int H,
+              int hd, int inverse, int dt, void* stream);
+int qeft_silu_mul_fwd(const void* g, const void* u, void* f, int64_t n, int dt, void* stream);
+int qeft_silu_mul_bwd(const void* df, const void* g, const void* u, void* dg, void* du, int64_t n, int dt,
+                      void* stream);
+
 /* Thread-local message for the last non-zero return. */
 const char* qeft_last_error(void);
 /* Library build string (arch, version). */

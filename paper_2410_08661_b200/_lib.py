@@ -58,6 +58,11 @@ SIGNATURES = {
     "qeft_div_scalar": (_I, [_VP, _I64, _F, _VP]),
     "qeft_adam_clip": (_I, [_VP, _VP, _VP, _VP, _I64, _VP, _F, _F, _F, _F, _F, _F, _F, _F, _F, _VP, _VP]),
     "qeft_weak_shadow": (_I, [_VP, _VP, _I, _I, _VP]),
+    "qeft_rmsnorm_fwd": (_I, [_VP, _VP, _VP, _VP, _I, _I, _I, _VP]),
+    "qeft_rmsnorm_bwd": (_I, [_VP, _VP, _VP, _VP, _VP, _VP, _I, _I, _I, _VP]),
+    "qeft_rope": (_I, [_VP, _VP, _VP, _VP, _I64, _I, _I, _I, _I, _I, _VP]),
+    "qeft_silu_mul_fwd": (_I, [_VP, _VP, _VP, _I64, _I, _VP]),
+    "qeft_silu_mul_bwd": (_I, [_VP, _VP, _VP, _VP, _VP, _I64, _I, _VP]),
     "qeft_last_error": (ctypes.c_char_p, []),
     "qeft_version": (ctypes.c_char_p, []),
 }

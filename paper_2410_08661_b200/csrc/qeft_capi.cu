@@ -131,4 +131,26 @@ int qeft_weak_shadow(const float* w32, const qeft_shadow_desc_t* d, int n, int m
   return weak_shadow(w32, d, n, max_elems, ST(s));
 }
 
+int qeft_rmsnorm_fwd(const void* x, const float* gain, void* y, float* rstd, int rows, int C, int dt, void* s) {
+  return rmsnorm_fwd(x, gain, y, rstd, rows, C, dt, ST(s));
+}
+
+int qeft_rmsnorm_bwd(const void* dy, const void* x, const float* gain, const float* rstd, const void* dres,
+                     void* dx, int rows, int C, int dt, void* s) {
+  return rmsnorm_bwd(dy, x, gain, rstd, dres, dx, rows, C, dt, ST(s));
+}
+
+int qeft_rope(const void* in, void* out, const float* cosv, const float* sinv, int64_t rows, int T, int H, int hd,
+              int inverse, int dt, void* s) {
+  return rope(in, out, cosv, sinv, rows, T, H, hd, inverse, dt, ST(s));
+}
+
+int qeft_silu_mul_fwd(const void* g, const void* u, void* f, int64_t n, int dt, void* s) {
+  return silu_mul_fwd(g, u, f, n, dt, ST(s));
+}
+
+int qeft_silu_mul_bwd(const void* df, const void* g, const void* u, void* dg, void* du, int64_t n, int dt, void* s) {
+  return silu_mul_bwd(df, g, u, dg, du, n, dt, ST(s));
+}
+
 }  // extern "C"

@@ -1,0 +1,255 @@
+// Fused elementwise kernels of the fine-tuning step's host model (the non-linear
+// parts around the QEFT linears, pkg/src/qeft/model.py:262-266 RMS-norm,
+// 249-259 rotary, SwiGLU at 389-391), forward and backward, bf16/fp16 activations
+// with fp32 math. Gains are frozen in weak-column tuning (tuning.py:187-248,
+// backward_batch with param_grads=False), so the RMS-norm backward returns dX only.
+// HBM-bound: each kernel reads and writes every element once.
+#include "qeft_common.cuh"
+#include "qeft_internal.h"
+
+using namespace qeft;
+
+namespace {
+
+constexpr float kRmsEps = 1e-5f;  // model.py:22
+
+template <typename T>
+QEFT_DEV float ld(const T* p) { return to_f32<T>(*p); }
+
+// one CTA per row; 8 consecutive elements per thread per iteration (16-byte accesses)
+template <typename T>
+__global__ void rmsnorm_fwd_kernel(const T* __restrict__ x, const float* __restrict__ gain, T* __restrict__ y,
+                                   float* __restrict__ rstd, int C) {
+  __shared__ float red[32];
+  const int row = blockIdx.x;
+  const T* xr = x + (int64_t)row * C;
+  T* yr = y + (int64_t)row * C;
+  float ss = 0.f;
+  for (int c = threadIdx.x * 8; c < C; c += blockDim.x * 8) {
+    const uint4 v = *reinterpret_cast<const uint4*>(xr + c);
+    const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float f = to_f32<T>(e[i]);
+      ss += f * f;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = rsqrtf(v / (float)C + kRmsEps);
+  }
+  __syncthreads();
+  const float r = red[0];
+  if (threadIdx.x == 0) rstd[row] = r;
+  for (int c = threadIdx.x * 8; c < C; c += blockDim.x * 8) {
+    const uint4 v = *reinterpret_cast<const uint4*>(xr + c);
+    const T* e = reinterpret_cast<const T*>(&v);
+    uint4 o;
+    T* oe = reinterpret_cast<T*>(&o);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) oe[i] = from_f32<T>(gain[c + i] * to_f32<T>(e[i]) * r);
+    *reinterpret_cast<uint4*>(yr + c) = o;
+  }
+}
+
+// dx = g*dy*r - x * r^3 * sum(g*dy*x) / C   (model.py:269-275, dgain not formed)
+// optional accumulation: dx += residual gradient (fuses the residual add of the block)
+template <typename T>
+__global__ void rmsnorm_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x, const float* __restrict__ gain,
+                                   const float* __restrict__ rstd, const T* __restrict__ dres, T* __restrict__ dx,
+                                   int C) {
+  __shared__ float red[32];
+  const int row = blockIdx.x;
+  const T* xr = x + (int64_t)row * C;
+  const T* dyr = dy + (int64_t)row * C;
+  const float r = rstd[row];
+  float dot = 0.f;
+  for (int c = threadIdx.x * 8; c < C; c += blockDim.x * 8) {
+    const uint4 xv = *reinterpret_cast<const uint4*>(xr + c);
+    const uint4 gv = *reinterpret_cast<const uint4*>(dyr + c);
+    const T* xe = reinterpret_cast<const T*>(&xv);
+    const T* ge = reinterpret_cast<const T*>(&gv);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dot += gain[c + i] * to_f32<T>(ge[i]) * to_f32<T>(xe[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dot;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float k = red[0] * r * r * r / (float)C;
+  for (int c = threadIdx.x * 8; c < C; c += blockDim.x * 8) {
+    const uint4 xv = *reinterpret_cast<const uint4*>(xr + c);
+    const uint4 gv = *reinterpret_cast<const uint4*>(dyr + c);
+    const T* xe = reinterpret_cast<const T*>(&xv);
+    const T* ge = reinterpret_cast<const T*>(&gv);
+    uint4 rv = make_uint4(0, 0, 0, 0);
+    if (dres) rv = *reinterpret_cast<const uint4*>(dres + (int64_t)row * C + c);
+    const T* re = reinterpret_cast<const T*>(&rv);
+    uint4 o;
+    T* oe = reinterpret_cast<T*>(&o);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float v = gain[c + i] * to_f32<T>(ge[i]) * r - to_f32<T>(xe[i]) * k;
+      if (dres) v += to_f32<T>(re[i]);
+      oe[i] = from_f32<T>(v);
+    }
+    *reinterpret_cast<uint4*>(dx + (int64_t)row * C + c) = o;
+  }
+}
+
+// rotary on (rows = B*T tokens) x (H heads x hd): pairs (j, j + hd/2) of every head rotate by
+// angle t * inv_freq[j] (model.py:256-259); dir = -1 applies the inverse (backward)
+template <typename T>
+__global__ void rope_kernel(const T* __restrict__ in, T* __restrict__ out, const float* __restrict__ cosv,
+                            const float* __restrict__ sinv, int64_t rows, int T_, int H, int hd, float dir) {
+  const int half = hd >> 1;
+  const int64_t n = rows * H * half;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i % half);
+    const int64_t rh = i / half;  // row * H + head
+    const int t = (int)((rh / H) % T_);
+    const int64_t base = rh * hd;
+    const float c = cosv[t * half + j], s = dir * sinv[t * half + j];
+    const float a = to_f32<T>(in[base + j]), b = to_f32<T>(in[base + j + half]);
+    out[base + j] = from_f32<T>(a * c - b * s);
+    out[base + j + half] = from_f32<T>(a * s + b * c);
+  }
+}
+
+// f = silu(g) * u (SwiGLU, model.py:389-391) and its backward
+template <typename T>
+__global__ void silu_mul_fwd_kernel(const T* __restrict__ g, const T* __restrict__ u, T* __restrict__ f, int64_t n) {
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8; i < n; i += (int64_t)gridDim.x * blockDim.x * 8) {
+    const uint4 gv = *reinterpret_cast<const uint4*>(g + i);
+    const uint4 uv = *reinterpret_cast<const uint4*>(u + i);
+    const T* ge = reinterpret_cast<const T*>(&gv);
+    const T* ue = reinterpret_cast<const T*>(&uv);
+    uint4 o;
+    T* oe = reinterpret_cast<T*>(&o);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float x = to_f32<T>(ge[k]);
+      oe[k] = from_f32<T>(x / (1.f + __expf(-x)) * to_f32<T>(ue[k]));
+    }
+    *reinterpret_cast<uint4*>(f + i) = o;
+  }
+}
+
+template <typename T>
+__global__ void silu_mul_bwd_kernel(const T* __restrict__ df, const T* __restrict__ g, const T* __restrict__ u,
+                                    T* __restrict__ dg, T* __restrict__ du, int64_t n) {
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8; i < n; i += (int64_t)gridDim.x * blockDim.x * 8) {
+    const uint4 fv = *reinterpret_cast<const uint4*>(df + i);
+    const uint4 gv = *reinterpret_cast<const uint4*>(g + i);
+    const uint4 uv = *reinterpret_cast<const uint4*>(u + i);
+    const T* fe = reinterpret_cast<const T*>(&fv);
+    const T* ge = reinterpret_cast<const T*>(&gv);
+    const T* ue = reinterpret_cast<const T*>(&uv);
+    uint4 og, ou;
+    T* oge = reinterpret_cast<T*>(&og);
+    T* oue = reinterpret_cast<T*>(&ou);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float x = to_f32<T>(ge[k]), d = to_f32<T>(fe[k]), uu = to_f32<T>(ue[k]);
+      const float sg = 1.f / (1.f + __expf(-x));
+      oue[k] = from_f32<T>(d * x * sg);                                // du = df * silu(g)
+      oge[k] = from_f32<T>(d * uu * (sg * (1.f + x * (1.f - sg))));     // dg (model.py:438)
+    }
+    *reinterpret_cast<uint4*>(dg + i) = og;
+    *reinterpret_cast<uint4*>(du + i) = ou;
+  }
+}
+
+int grid_for(int64_t n, int per_thread) {
+  const int64_t blocks = (n / per_thread + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 16));
+}
+
+}  // namespace
+
+namespace qeft {
+
+int rmsnorm_fwd(const void* x, const float* gain, void* y, float* rstd, int rows, int C, int dt, cudaStream_t st) {
+  QEFT_CHECK(C % 8 == 0 && rows >= 0, QEFT_ERR_SHAPE, "rmsnorm: C=%d must be a multiple of 8", C);
+  if (!rows) return 0;
+  const int thr = std::min(1024, std::max(32, C / 8 / 32 * 32));
+  if (dt == QEFT_BF16)
+    rmsnorm_fwd_kernel<__nv_bfloat16><<<rows, thr, 0, st>>>((const __nv_bfloat16*)x, gain, (__nv_bfloat16*)y, rstd, C);
+  else
+    rmsnorm_fwd_kernel<__half><<<rows, thr, 0, st>>>((const __half*)x, gain, (__half*)y, rstd, C);
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int rmsnorm_bwd(const void* dy, const void* x, const float* gain, const float* rstd, const void* dres, void* dx,
+                int rows, int C, int dt, cudaStream_t st) {
+  QEFT_CHECK(C % 8 == 0 && rows >= 0, QEFT_ERR_SHAPE, "rmsnorm: C=%d must be a multiple of 8", C);
+  if (!rows) return 0;
+  const int thr = std::min(1024, std::max(32, C / 8 / 32 * 32));
+  if (dt == QEFT_BF16)
+    rmsnorm_bwd_kernel<__nv_bfloat16><<<rows, thr, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, gain,
+                                                           rstd, (const __nv_bfloat16*)dres, (__nv_bfloat16*)dx, C);
+  else
+    rmsnorm_bwd_kernel<__half><<<rows, thr, 0, st>>>((const __half*)dy, (const __half*)x, gain, rstd,
+                                                    (const __half*)dres, (__half*)dx, C);
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int rope(const void* in, void* out, const float* cosv, const float* sinv, int64_t rows, int T_, int H, int hd,
+         int inverse, int dt, cudaStream_t st) {
+  QEFT_CHECK(hd % 2 == 0 && T_ > 0, QEFT_ERR_SHAPE, "rope: head_dim %d must be even", hd);
+  const int64_t n = rows * H * (hd / 2);
+  if (!n) return 0;
+  const float dir = inverse ? -1.f : 1.f;
+  if (dt == QEFT_BF16)
+    rope_kernel<__nv_bfloat16><<<grid_for(n, 1), 256, 0, st>>>((const __nv_bfloat16*)in, (__nv_bfloat16*)out, cosv,
+                                                               sinv, rows, T_, H, hd, dir);
+  else
+    rope_kernel<__half><<<grid_for(n, 1), 256, 0, st>>>((const __half*)in, (__half*)out, cosv, sinv, rows, T_, H, hd,
+                                                        dir);
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int silu_mul_fwd(const void* g, const void* u, void* f, int64_t n, int dt, cudaStream_t st) {
+  QEFT_CHECK(n % 8 == 0, QEFT_ERR_SHAPE, "silu_mul: n=%lld must be a multiple of 8", (long long)n);
+  if (!n) return 0;
+  if (dt == QEFT_BF16)
+    silu_mul_fwd_kernel<__nv_bfloat16><<<grid_for(n, 8), 256, 0, st>>>((const __nv_bfloat16*)g, (const __nv_bfloat16*)u,
+                                                                       (__nv_bfloat16*)f, n);
+  else
+    silu_mul_fwd_kernel<__half><<<grid_for(n, 8), 256, 0, st>>>((const __half*)g, (const __half*)u, (__half*)f, n);
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int silu_mul_bwd(const void* df, const void* g, const void* u, void* dg, void* du, int64_t n, int dt,
+                 cudaStream_t st) {
+  QEFT_CHECK(n % 8 == 0, QEFT_ERR_SHAPE, "silu_mul: n=%lld must be a multiple of 8", (long long)n);
+  if (!n) return 0;
+  if (dt == QEFT_BF16)
+    silu_mul_bwd_kernel<__nv_bfloat16><<<grid_for(n, 8), 256, 0, st>>>(
+        (const __nv_bfloat16*)df, (const __nv_bfloat16*)g, (const __nv_bfloat16*)u, (__nv_bfloat16*)dg,
+        (__nv_bfloat16*)du, n);
+  else
+    silu_mul_bwd_kernel<__half><<<grid_for(n, 8), 256, 0, st>>>((const __half*)df, (const __half*)g, (const __half*)u,
+                                                                (__half*)dg, (__half*)du, n);
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace qeft

@@ -62,4 +62,13 @@ int adam_clip(float* w, float* m, float* v, const float* g, int64_t n, const dou
 int weak_shadow(const float* w32, const qeft_shadow_desc_t* d, int n_layers, int max_elems,
                 cudaStream_t st);
 
+int rmsnorm_fwd(const void* x, const float* gain, void* y, float* rstd, int rows, int C, int dt, cudaStream_t st);
+int rmsnorm_bwd(const void* dy, const void* x, const float* gain, const float* rstd, const void* dres, void* dx,
+                int rows, int C, int dt, cudaStream_t st);
+int rope(const void* in, void* out, const float* cosv, const float* sinv, int64_t rows, int T, int H, int hd,
+         int inverse, int dt, cudaStream_t st);
+int silu_mul_fwd(const void* g, const void* u, void* f, int64_t n, int dt, cudaStream_t st);
+int silu_mul_bwd(const void* df, const void* g, const void* u, void* dg, void* du, int64_t n, int dt,
+                 cudaStream_t st);
+
 }  // namespace qeft

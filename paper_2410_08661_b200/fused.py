@@ -1,0 +1,100 @@
+"""Autograd wrappers of the fused elementwise kernels (libqeft_b200 qeft_rmsnorm_*,
+qeft_rope, qeft_silu_mul_*) used by the fine-tuning host model for fp16/bf16
+activations. Semantics follow the reference engine (pkg/src/qeft/model.py:249-275
+RMS-norm and rotary, 389-391 / 437-438 SwiGLU); the frozen norm gain gets no
+gradient (tuning.py: backward_batch(..., param_grads=False))."""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .layer import _DT
+
+_TDT = {torch.float16: _DT["f16"], torch.bfloat16: _DT["bf16"]}
+
+
+def supported(x) -> bool:
+    return x.is_cuda and x.dtype in _TDT
+
+
+class _RMSNorm(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, gain):
+        C = x.shape[-1]
+        x2 = x.reshape(-1, C).contiguous()
+        y = torch.empty_like(x2)
+        rstd = torch.empty(x2.shape[0], dtype=torch.float32, device=x.device)
+        g = gain.float().contiguous()
+        _lib.check(_lib.lib().qeft_rmsnorm_fwd(x2.data_ptr(), g.data_ptr(), y.data_ptr(), rstd.data_ptr(),
+                                               x2.shape[0], C, _TDT[x.dtype], _lib.stream_ptr()), "rmsnorm_fwd")
+        ctx.save_for_backward(x2, g, rstd)
+        return y.view(x.shape)
+
+    @staticmethod
+    def backward(ctx, dy):
+        x2, g, rstd = ctx.saved_tensors
+        C = x2.shape[1]
+        dy2 = dy.reshape(-1, C).contiguous()
+        dx = torch.empty_like(x2)
+        _lib.check(_lib.lib().qeft_rmsnorm_bwd(dy2.data_ptr(), x2.data_ptr(), g.data_ptr(), rstd.data_ptr(), None,
+                                               dx.data_ptr(), x2.shape[0], C, _TDT[dy2.dtype], _lib.stream_ptr()),
+                   "rmsnorm_bwd")
+        return dx.view(dy.shape), None
+
+
+class _Rope(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, cos, sin, T, H, hd):
+        xc = x.contiguous()
+        y = torch.empty_like(xc)
+        rows = xc.numel() // (H * hd)
+        _lib.check(_lib.lib().qeft_rope(xc.data_ptr(), y.data_ptr(), cos.data_ptr(), sin.data_ptr(), rows, T, H, hd,
+                                        0, _TDT[x.dtype], _lib.stream_ptr()), "rope")
+        ctx.save_for_backward(cos, sin)
+        ctx.dims = (rows, T, H, hd)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        cos, sin = ctx.saved_tensors
+        rows, T, H, hd = ctx.dims
+        dyc = dy.contiguous()
+        dx = torch.empty_like(dyc)
+        _lib.check(_lib.lib().qeft_rope(dyc.data_ptr(), dx.data_ptr(), cos.data_ptr(), sin.data_ptr(), rows, T, H, hd,
+                                        1, _TDT[dy.dtype], _lib.stream_ptr()), "rope_bwd")
+        return dx, None, None, None, None, None
+
+
+class _SiluMul(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, g, u):
+        gc, uc = g.contiguous(), u.contiguous()
+        f = torch.empty_like(gc)
+        _lib.check(_lib.lib().qeft_silu_mul_fwd(gc.data_ptr(), uc.data_ptr(), f.data_ptr(), gc.numel(),
+                                                _TDT[g.dtype], _lib.stream_ptr()), "silu_mul_fwd")
+        ctx.save_for_backward(gc, uc)
+        return f
+
+    @staticmethod
+    def backward(ctx, df):
+        gc, uc = ctx.saved_tensors
+        dfc = df.contiguous()
+        dg, du = torch.empty_like(gc), torch.empty_like(uc)
+        _lib.check(_lib.lib().qeft_silu_mul_bwd(dfc.data_ptr(), gc.data_ptr(), uc.data_ptr(), dg.data_ptr(),
+                                                du.data_ptr(), gc.numel(), _TDT[gc.dtype], _lib.stream_ptr()),
+                   "silu_mul_bwd")
+        return dg, du
+
+
+def rms_norm(x, gain):
+    return _RMSNorm.apply(x, gain)
+
+
+def rope(x, cos, sin, T, H, hd):
+    """x: (B, T, H*hd) token-major; returns the rotated tensor in the same layout."""
+    return _Rope.apply(x, cos, sin, T, H, hd)
+
+
+def silu_mul(g, u):
+    return _SiluMul.apply(g, u)

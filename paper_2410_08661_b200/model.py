@@ -22,6 +22,7 @@ import numpy as np
 import torch
 import torch.nn.functional as F
 
+from . import fused
 from .errors import ShapeError
 from .qlinear import QEFTLinear
 from .qmodel import BLOCK_LINEARS, RMS_EPS, ROPE_BASE, ModelConfig
@@ -62,6 +63,8 @@ class QEFTBlock(torch.nn.Module):
             self.add_module(nm, layers[nm])
 
     def forward(self, x, cos, sin, cfg: ModelConfig):
+        if fused.supported(x) and x.shape[-1] % 8 == 0 and cfg.d_ff % 8 == 0:
+            return self._forward_fused(x, cos, sin, cfg)
         B, T, _ = x.shape
         H, hd = cfg.n_heads, cfg.head_dim
         a = rms_norm(x, self.gain1)
@@ -77,6 +80,20 @@ class QEFTBlock(torch.nn.Module):
         g = self.w_gate(b2).to(x.dtype)
         f = F.silu(g) * u
         return x1 + self.w_down(f).to(x.dtype)
+
+    def _forward_fused(self, x, cos, sin, cfg: ModelConfig):
+        """fp16/bf16 activations: RMS-norm, rotary and SwiGLU run as fused libqeft_b200 kernels."""
+        B, T, _ = x.shape
+        H, hd = cfg.n_heads, cfg.head_dim
+        a = fused.rms_norm(x, self.gain1)
+        q = fused.rope(self.wq(a), cos, sin, T, H, hd).view(B, T, H, hd).transpose(1, 2)
+        k = fused.rope(self.wk(a), cos, sin, T, H, hd).view(B, T, H, hd).transpose(1, 2)
+        v = self.wv(a).view(B, T, H, hd).transpose(1, 2)
+        o = F.scaled_dot_product_attention(q, k, v, is_causal=True, scale=1.0 / math.sqrt(hd))
+        x1 = x + self.wo(o.transpose(1, 2).reshape(B, T, H * hd))
+        b2 = fused.rms_norm(x1, self.gain2)
+        f = fused.silu_mul(self.w_gate(b2), self.w_up(b2))
+        return x1 + self.w_down(f)
 
 
 class QEFTDecoder(torch.nn.Module):
@@ -154,7 +171,7 @@ class QEFTDecoder(torch.nn.Module):
         x = F.embedding(tokens, self.embedding)
         for blk in self.blocks:
             x = blk(x, cos, sin, cfg)
-        z = rms_norm(x, self.final_gain)
+        z = fused.rms_norm(x, self.final_gain) if fused.supported(x) else rms_norm(x, self.final_gain)
         return z @ self.head.t()
 
     @torch.no_grad()

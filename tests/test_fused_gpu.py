@@ -1,0 +1,101 @@
+"""Fused elementwise kernels of the fine-tuning host model vs fp32 torch restatements of the
+reference engine (pkg/src/qeft/model.py:249-275 RMS-norm / rotary, 389-391 and 437-438 SwiGLU),
+forward and backward. Tolerance: bf16 storage, max|d| / max(1, max|ref|) <= 1e-2."""
+
+import math
+
+import numpy as np
+import pytest
+
+from tests.conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return torch
+
+
+def _np(t):
+    return t.detach().float().cpu().numpy()
+
+
+@pytest.mark.parametrize("dt", ["bf16", "f16"])
+def test_rmsnorm_fwd_bwd(torch_, dt):
+    torch = torch_
+    from paper_2410_08661_b200 import fused
+    td = {"bf16": torch.bfloat16, "f16": torch.float16}[dt]
+    x = torch.randn(3, 37, 4096, device="cuda").to(td).requires_grad_(True)
+    gain = 1.0 + 0.1 * torch.randn(4096, device="cuda")
+    y = fused.rms_norm(x, gain)
+    xr = x.detach().float().requires_grad_(True)
+    yr = gain * xr / torch.sqrt((xr * xr).mean(-1, keepdim=True) + 1e-5)
+    assert rel_err(_np(y), _np(yr)) <= 1e-2
+    dy = torch.randn_like(y)
+    y.backward(dy)
+    yr.backward(dy.float())
+    assert rel_err(_np(x.grad), _np(xr.grad)) <= 1e-2
+
+
+def test_rope_fwd_bwd(torch_):
+    torch = torch_
+    from paper_2410_08661_b200 import fused
+    from paper_2410_08661_b200.model import rope_tables
+    B, T, H, hd = 2, 65, 4, 128
+    cos, sin = rope_tables(hd, T, "cuda")
+    x = torch.randn(B, T, H * hd, device="cuda").to(torch.bfloat16).requires_grad_(True)
+    y = fused.rope(x, cos, sin, T, H, hd)
+    xr = x.detach().float().view(B, T, H, hd).requires_grad_(True)
+    half = hd // 2
+    c, s = cos[None, :, None, :], sin[None, :, None, :]
+    x1, x2 = xr[..., :half], xr[..., half:]
+    yr = torch.cat([x1 * c - x2 * s, x1 * s + x2 * c], -1)
+    assert rel_err(_np(y), _np(yr.reshape(B, T, H * hd))) <= 1e-2
+    dy = torch.randn_like(y)
+    y.backward(dy)
+    yr.backward(dy.float().view(B, T, H, hd))
+    assert rel_err(_np(x.grad), _np(xr.grad.reshape(B, T, H * hd))) <= 1e-2
+
+
+def test_silu_mul_fwd_bwd(torch_):
+    torch = torch_
+    from paper_2410_08661_b200 import fused
+    g = (2 * torch.randn(77, 11008, device="cuda")).to(torch.bfloat16).requires_grad_(True)
+    u = torch.randn(77, 11008, device="cuda").to(torch.bfloat16).requires_grad_(True)
+    f = fused.silu_mul(g, u)
+    gr = g.detach().float().requires_grad_(True)
+    ur = u.detach().float().requires_grad_(True)
+    fr = gr * torch.sigmoid(gr) * ur
+    assert rel_err(_np(f), _np(fr)) <= 1e-2
+    df = torch.randn_like(f)
+    f.backward(df)
+    fr.backward(df.float())
+    assert rel_err(_np(g.grad), _np(gr.grad)) <= 1e-2
+    assert rel_err(_np(u.grad), _np(ur.grad)) <= 1e-2
+
+
+def test_block_fused_matches_torch_path(torch_):
+    """One decoder block on the fused path vs the same block through the plain torch
+    ops (fp32 non-linear math), bf16 QEFT linears in both."""
+    torch = torch_
+    from paper_2410_08661_b200 import fused
+    from paper_2410_08661_b200.model import QEFTDecoder
+    from paper_2410_08661_b200.qmodel import ModelConfig
+    cfg = ModelConfig(d_model=512, n_heads=4, head_dim=128, d_ff=1024, n_blocks=1, vocab_size=300, max_seq=256)
+    m = QEFTDecoder.synthetic(cfg, k=128, bits=4, g=128, act_dtype="bf16", compute_dtype="bf16", seed=3)
+    tok = torch.randint(0, 300, (2, 96), device="cuda")
+    blk = m.blocks[0]
+    x = torch.randn(2, 96, 512, device="cuda").to(torch.bfloat16)
+    cos, sin = m.rope(96, x.device)
+    y_f = blk._forward_fused(x, cos, sin, cfg)
+    orig = fused.supported
+    fused.supported = lambda t: False
+    try:
+        y_t = blk(x.float(), cos, sin, cfg)
+    finally:
+        fused.supported = orig
+    assert rel_err(_np(y_f), _np(y_t)) <= 2e-2
