@@ -111,21 +111,37 @@ __global__ void rmsnorm_bwd_kernel(const T* __restrict__ dy, const T* __restrict
 }
 
 // rotary on (rows = B*T tokens) x (H heads x hd): pairs (j, j + hd/2) of every head rotate by
-// angle t * inv_freq[j] (model.py:256-259); dir = -1 applies the inverse (backward)
+// angle t * inv_freq[j] (model.py:256-259); dir = -1 applies the inverse (backward).
+// One CTA per token row: the row's cos/sin are read once, 8 pairs per thread-iteration with
+// 16-byte accesses (hd/2 % 8 == 0).
 template <typename T>
 __global__ void rope_kernel(const T* __restrict__ in, T* __restrict__ out, const float* __restrict__ cosv,
-                            const float* __restrict__ sinv, int64_t rows, int T_, int H, int hd, float dir) {
+                            const float* __restrict__ sinv, int T_, int H, int hd, float dir) {
   const int half = hd >> 1;
-  const int64_t n = rows * H * half;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int j = (int)(i % half);
-    const int64_t rh = i / half;  // row * H + head
-    const int t = (int)((rh / H) % T_);
-    const int64_t base = rh * hd;
-    const float c = cosv[t * half + j], s = dir * sinv[t * half + j];
-    const float a = to_f32<T>(in[base + j]), b = to_f32<T>(in[base + j + half]);
-    out[base + j] = from_f32<T>(a * c - b * s);
-    out[base + j + half] = from_f32<T>(a * s + b * c);
+  const int64_t row = blockIdx.x;
+  const int t = (int)(row % T_);
+  const float* cr = cosv + (int64_t)t * half;
+  const float* sr = sinv + (int64_t)t * half;
+  const int chunks = half >> 3;  // 8-pair chunks per head
+  for (int e = threadIdx.x; e < H * chunks; e += blockDim.x) {
+    const int h = e / chunks, j = (e - h * chunks) * 8;
+    const int64_t base = (row * H + h) * hd;
+    const uint4 av = *reinterpret_cast<const uint4*>(in + base + j);
+    const uint4 bv = *reinterpret_cast<const uint4*>(in + base + j + half);
+    const T* ae = reinterpret_cast<const T*>(&av);
+    const T* be = reinterpret_cast<const T*>(&bv);
+    uint4 oa, ob;
+    T* oae = reinterpret_cast<T*>(&oa);
+    T* obe = reinterpret_cast<T*>(&ob);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float c = cr[j + i], s = dir * sr[j + i];
+      const float a = to_f32<T>(ae[i]), b = to_f32<T>(be[i]);
+      oae[i] = from_f32<T>(a * c - b * s);
+      obe[i] = from_f32<T>(a * s + b * c);
+    }
+    *reinterpret_cast<uint4*>(out + base + j) = oa;
+    *reinterpret_cast<uint4*>(out + base + j + half) = ob;
   }
 }
 
@@ -211,16 +227,15 @@ int rmsnorm_bwd(const void* dy, const void* x, const float* gain, const float* r
 
 int rope(const void* in, void* out, const float* cosv, const float* sinv, int64_t rows, int T_, int H, int hd,
          int inverse, int dt, cudaStream_t st) {
-  QEFT_CHECK(hd % 2 == 0 && T_ > 0, QEFT_ERR_SHAPE, "rope: head_dim %d must be even", hd);
-  const int64_t n = rows * H * (hd / 2);
-  if (!n) return 0;
+  QEFT_CHECK(hd % 16 == 0 && T_ > 0, QEFT_ERR_SHAPE, "rope: head_dim %d must be a multiple of 16", hd);
+  if (!rows) return 0;
   const float dir = inverse ? -1.f : 1.f;
+  const int thr = std::min(256, std::max(32, H * (hd / 16)));
   if (dt == QEFT_BF16)
-    rope_kernel<__nv_bfloat16><<<grid_for(n, 1), 256, 0, st>>>((const __nv_bfloat16*)in, (__nv_bfloat16*)out, cosv,
-                                                               sinv, rows, T_, H, hd, dir);
+    rope_kernel<__nv_bfloat16><<<(unsigned)rows, thr, 0, st>>>((const __nv_bfloat16*)in, (__nv_bfloat16*)out, cosv,
+                                                               sinv, T_, H, hd, dir);
   else
-    rope_kernel<__half><<<grid_for(n, 1), 256, 0, st>>>((const __half*)in, (__half*)out, cosv, sinv, rows, T_, H, hd,
-                                                        dir);
+    rope_kernel<__half><<<(unsigned)rows, thr, 0, st>>>((const __half*)in, (__half*)out, cosv, sinv, T_, H, hd, dir);
   QEFT_CUDA(cudaGetLastError());
   return 0;
 }
