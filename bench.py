@@ -38,8 +38,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "QEFT decode GEMV HBM GB/s (% peak); fine-tune tokens/s at 1/2/4/8 B200"
-WORKLOAD = ("LLaMA-2-7B-shaped decoder layer stack (32 blocks x 7 linears = 224 GEMVs), "
-            "4-bit QEFT g=128 k=128, decode GEMV batch 1")
+def workload(blocks=32, n_cols=1):
+    return (f"LLaMA-2-7B-shaped decoder layer stack ({blocks} blocks x 7 linears = {7 * blocks} GEMVs), "
+            f"4-bit QEFT g=128 k=128, decode GEMV batch {n_cols}")
+
+
+WORKLOAD = workload()
 BLOCK_SHAPES = [(4096, 4096), (4096, 4096), (4096, 4096), (4096, 4096),
                 (11008, 4096), (11008, 4096), (4096, 11008)]
 
@@ -211,10 +215,17 @@ def kernel_roofline(torch, n_blocks, peak, n_cols):
 def run_b200(args):
     import torch
     ws, rank, local = _dist()
-    torch.cuda.set_device(local)
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL over NVLink; QEFT_DIST_BACKEND=gloo only to exercise the multi-rank logic with
+        # several ranks on one GPU (NCCL refuses duplicate devices)
+        backend = os.environ.get("QEFT_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     from paper_2410_08661_b200.decode import LinearStack, llama_stack_layers
     peak, peak_kind = _peaks()
     n = args.n_cols
@@ -231,7 +242,7 @@ def run_b200(args):
 
     barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
@@ -270,7 +281,7 @@ def run_b200(args):
     n_layers = len(layers)
     del stack, layers
     torch.cuda.empty_cache()
-    ft = None if args.no_ft else finetune_bench(args, ws, rank, local, torch)
+    ft = None if args.no_ft else finetune_bench(args, ws, rank, dev, torch)
     line = None
     if rank == 0:
         count = {(4096, 4096): 4, (11008, 4096): 2, (4096, 11008): 1}
@@ -289,7 +300,7 @@ def run_b200(args):
             "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD, "n_cols": n, "blocks": args.blocks,
+            "config": {"workload": workload(args.blocks, n), "n_cols": n, "blocks": args.blocks,
                        "gemv_per_step": n_layers, "bytes_per_step": bytes_step,
                        "l2": "inputs larger than L2 (%.2f GB of weights per step)" % (bytes_step / 1e9),
                        "parallelism": f"replicas{ws}"},
