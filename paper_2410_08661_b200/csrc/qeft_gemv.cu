@@ -22,11 +22,12 @@
 //     the programmatic-dependent-launch wait, so a layer's weight stream
 //     overlaps the previous kernel; only x (staged once into shared memory in
 //     the B200 K order, zero padded) and the trainable weak block wait for it.
-//   * Codes become (magic + code) half2 A fragments with one LOP3 each; a
-//     second MMA with an all-ones A fragment yields sum(x) in the accumulator
-//     layout, so the per-group fold
+//   * Codes become (magic + code) half2 A fragments with one LOP3 each and the
+//     per-group fold is
 //       y += s' * acc + (z - magic * s') * sum(x)   (s' = s, or s/16 for the
-//     fp16 hi-nibble trick) needs no separate pass over x. GT (64-column steps
+//     fp16 hi-nibble trick). For N <= 8 the group sums of x are formed while x is
+//     staged (segmented warp shuffles) and read from shared memory; for N > 8 an
+//     all-ones MMA per step accumulates them in the accumulator layout. GT (64-column steps
 //     per group) is a template constant; GT = 0 is the generic per-element
 //     dequant path for group sizes that are not 64 * {1, 2, 4}.
 #include <algorithm>
@@ -121,6 +122,10 @@ int env_int(const char* name, int dflt) {
   return v ? atoi(v) : dflt;
 }
 
+__host__ __device__ inline size_t xsum_bytes(int ng, int nt) {
+  return ((size_t)ng * nt * 8 * sizeof(float) + 127) & ~(size_t)127;
+}
+
 template <int GT>
 struct Ring {
   static constexpr int G = GT > 0 ? GT : 1;
@@ -137,6 +142,8 @@ gemv_kernel(const GemvArgs a) {
   __shared__ __align__(8) uint64_t wbar[2];
   constexpr bool FOLD = GT > 0;
   constexpr int G = Ring<GT>::G, kSP = Ring<GT>::kSP, kSlot = Ring<GT>::kSlot;
+  // sum(x) per group: from the x staging for one n-tile (N <= 8), else an all-ones MMA per step
+  constexpr bool kXsum = FOLD && NT == 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g8 = lane >> 2, t4 = lane & 3;
   const int s_beg = min(warp * a.spw, a.nsq), s_end = min(s_beg + a.spw, a.nsq);
@@ -146,7 +153,9 @@ gemv_kernel(const GemvArgs a) {
   const int nrbc = (a.n_rb - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
   const int nwt = a.k_pad >> 6;
   const uint32_t wbytes = (uint32_t)nwt * 2048u;
-  uint8_t* wsm = smem + (XS ? (size_t)a.n * a.xs_ld * sizeof(T) : 0);
+  // per-(group, column) sums of x: the zero-point term of the fold, shared by every row
+  float* xsum = reinterpret_cast<float*>(smem + (XS ? (size_t)a.n * a.xs_ld * sizeof(T) : 0));
+  uint8_t* wsm = reinterpret_cast<uint8_t*>(xsum) + xsum_bytes(a.ng, NT);
   uint8_t* ring = wsm + 2 * wbytes + (size_t)warp * kR * kSlot;
 
   auto rb_of = [&](int j) { return (int)blockIdx.x + j * (int)gridDim.x; };
@@ -197,12 +206,37 @@ gemv_kernel(const GemvArgs a) {
     return *reinterpret_cast<uint32_t*>(&r);
   };
 
+  // fold group `grp`: acc += s' * g + (z - magic * s') * sum(x of the group)
+  // fold group `grp`: acc += s' * g + (z - magic * s') * sum(x); the sums come from the
+  // staging table (kXsum) or from the all-ones MMA accumulators `xs`
+  auto fold = [&](const float2* szs, int grp, const float (&g)[NT][4], const float (&xs)[NT][4]) {
+    constexpr float M = DTraits<T>::kMagicF;
+    const float2 p0 = szs[g8], p1 = szs[g8 + 8];
+    const float s0 = p0.x;
+    const float s1 = (BITS == 4 && DTraits<T>::kHiTrick) ? p1.x * (1.f / 16.f) : p1.x;
+    const float z0 = p0.y - M * s0, z1 = p1.y - M * s1;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      float2 sx0, sx1;
+      if constexpr (kXsum) {
+        sx0 = sx1 = *reinterpret_cast<const float2*>(xsum + grp * (NT * 8) + 8 * nt + 2 * t4);
+      } else {
+        sx0 = make_float2(xs[nt][0], xs[nt][1]);
+        sx1 = make_float2(xs[nt][2], xs[nt][3]);
+      }
+      acc[nt][0] += s0 * g[nt][0] + z0 * sx0.x;
+      acc[nt][1] += s0 * g[nt][1] + z0 * sx0.y;
+      acc[nt][2] += s1 * g[nt][2] + z1 * sx1.x;
+      acc[nt][3] += s1 * g[nt][3] + z1 * sx1.y;
+    }
+  };
+
   // one 64-column step: decode + MMA (+ fold with params p0/p1 when `fold_now`)
   auto step = [&](int rb, int st, const uint4& q, const float2* szs, bool fold_now) {
     const int col = st * 64;
     uint4 xa[NT], xb[NT];
     x_frag(col, xa, xb);
-    if constexpr (FOLD) {
+    if constexpr (FOLD && !kXsum) {
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -244,21 +278,13 @@ gemv_kernel(const GemvArgs a) {
         mma16816<T>(FOLD ? accg[nt] : acc[nt], f[j], b0_, b1_);
       }
     if constexpr (FOLD) {
-      if (fold_now) {
-        constexpr float M = DTraits<T>::kMagicF;
-        const float2 p0 = szs[g8], p1 = szs[g8 + 8];
-        const float s0 = p0.x;
-        const float s1 = (BITS == 4 && DTraits<T>::kHiTrick) ? p1.x * (1.f / 16.f) : p1.x;
-        const float z0 = p0.y - M * s0, z1 = p1.y - M * s1;
+      // steps past the last group (g = 64 with an odd group count) carry only padding
+      if (fold_now && st / G < a.ng) {
+        fold(szs, st / G, accg, accx);
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          acc[nt][0] += s0 * accg[nt][0] + z0 * accx[nt][0];
-          acc[nt][1] += s0 * accg[nt][1] + z0 * accx[nt][1];
-          acc[nt][2] += s1 * accg[nt][2] + z1 * accx[nt][2];
-          acc[nt][3] += s1 * accg[nt][3] + z1 * accx[nt][3];
+        for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
           for (int e = 0; e < 4; ++e) accg[nt][e] = accx[nt][e] = 0.f;
-        }
       }
     }
   };
@@ -329,21 +355,6 @@ gemv_kernel(const GemvArgs a) {
       }
     }
   };
-  // fold group partials (g = sum (magic + c) x, xs = sum x) with the group's params
-  auto fold = [&](const float2* szs, const float (&g)[NT][4], const float (&xs)[NT][4]) {
-    constexpr float M = DTraits<T>::kMagicF;
-    const float2 p0 = szs[g8], p1 = szs[g8 + 8];
-    const float s0 = p0.x;
-    const float s1 = (BITS == 4 && DTraits<T>::kHiTrick) ? p1.x * (1.f / 16.f) : p1.x;
-    const float z0 = p0.y - M * s0, z1 = p1.y - M * s1;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      acc[nt][0] += s0 * g[nt][0] + z0 * xs[nt][0];
-      acc[nt][1] += s0 * g[nt][1] + z0 * xs[nt][1];
-      acc[nt][2] += s1 * g[nt][2] + z1 * xs[nt][2];
-      acc[nt][3] += s1 * g[nt][3] + z1 * xs[nt][3];
-    }
-  };
   auto compute = [&](int t, int j, int b) {
     const uint8_t* slot = ring + (t % kR) * kSlot;
     const int rb = rb_of(j);
@@ -370,7 +381,7 @@ gemv_kernel(const GemvArgs a) {
           for (int nt = 0; nt < NT; ++nt) {
             uint32_t b0_, b1_;
             bsel(xa[nt], xb[nt], jj, b0_, b1_);
-            if constexpr (FOLD) mma16816<T>(ax[u][nt], ones, b0_, b1_);
+            if constexpr (FOLD && !kXsum) mma16816<T>(ax[u][nt], ones, b0_, b1_);
             mma16816<T>(ag[u][nt], f[jj], b0_, b1_);
           }
       }
@@ -386,11 +397,12 @@ gemv_kernel(const GemvArgs a) {
 #pragma unroll
             for (int u = 1; u < G; ++u) {
               g[nt][e] += ag[i * G + u][nt][e];
-              xs[nt][e] += ax[i * G + u][nt][e];
+              if constexpr (!kXsum) xs[nt][e] += ax[i * G + u][nt][e];
             }
           }
         if constexpr (FOLD) {
-          fold(reinterpret_cast<const float2*>(slot + kU * 512 + i * 128), g, xs);
+          const int grp = (b0 + i * G) / G;
+          if (grp < a.ng) fold(reinterpret_cast<const float2*>(slot + kU * 512 + i * 128), grp, g, xs);
         } else {
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt)
@@ -436,7 +448,45 @@ gemv_kernel(const GemvArgs a) {
     issue_weak(0);
     issue_weak(1);
   }
-  if constexpr (XS) {
+  if constexpr (kXsum) {
+    // Stage x once per CTA (B200 K order, zero padded) and form the per-(group, column) sums
+    // of x on the way: the quantized columns are walked in 8-column chunks (all n <= 8 columns'
+    // loads in flight together); a group's 8 * G chunks are consecutive lanes of one warp, so a
+    // segmented shuffle reduction gives its fp32 sum without another pass over x.
+    constexpr int kCG = 8 * G;  // chunks per group (<= 32)
+    const int qchunks = a.m_pad >> 3, row_chunks = (a.m_pad + a.k_pad) >> 3;
+    using T2 = typename DTraits<T>::T2;
+    for (int c0 = 0; c0 < row_chunks; c0 += kThreads) {
+      const int c = c0 + (int)threadIdx.x;
+      uint4 v[8];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        v[n] = make_uint4(0, 0, 0, 0);
+        if (n < a.n && c < row_chunks) v[n] = x_chunk<T>(a, n, c << 3);
+      }
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        if (n >= a.n) break;
+        if (XS && c < row_chunks) *reinterpret_cast<uint4*>(reinterpret_cast<T*>(smem) + n * a.xs_ld + (c << 3)) = v[n];
+        if (c0 < qchunks) {  // warp-uniform: qchunks is a multiple of 16, kThreads of 32
+          const T2* h = reinterpret_cast<const T2*>(&v[n]);
+          float sum = 0.f;
+          if (c < qchunks) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float2 f2 = t2_to_f2<T2>(h[q]);
+              sum += f2.x + f2.y;
+            }
+          }
+#pragma unroll
+          for (int o = 1; o < kCG; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+          const int grp = c / kCG;
+          if ((c % kCG) == 0 && c < qchunks && grp < a.ng) xsum[grp * (NT * 8) + n] = sum;
+        }
+      }
+    }
+    __syncthreads();
+  } else if constexpr (XS) {
     const int row_chunks = (a.m_pad + a.k_pad) >> 3;
     for (int e = threadIdx.x; e < a.n * row_chunks; e += kThreads) {
       const int n = e / row_chunks, jj = (e - n * row_chunks) << 3;
@@ -517,7 +567,7 @@ int launch(const GemvArgs& a0, cudaStream_t st) {
   const size_t ring_bytes = (size_t)kWarps * kR * Ring<GT>::kSlot;
   const bool xs = xs_bytes <= (size_t)kXSmemMax;
   a.xs_ld = xs ? a.m_pad + a.k_pad + 8 : 0;  // 16 B skew between rows: conflict-free LDS.128
-  const size_t smem = (xs ? xs_bytes : 0) + w_bytes + ring_bytes;
+  const size_t smem = (xs ? xs_bytes : 0) + xsum_bytes(a.ng, NT) + w_bytes + ring_bytes;
   QEFT_CHECK(smem <= 200 * 1024, QEFT_ERR_LAYOUT, "gemv: k_pad=%d too large", a.k_pad);
   // persistent CTAs: as many per SM as shared memory allows (<= 2: registers),
   // equal row-block counts per CTA
