@@ -226,12 +226,15 @@ def run_b200(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             dist.init_process_group(backend)
-    from paper_2410_08661_b200.decode import LinearStack, llama_stack_layers
+    from paper_2410_08661_b200.decode import LinearStack, llama_launch_groups, llama_stack_layers
     peak, peak_kind = _peaks()
     n = args.n_cols
 
     layers = llama_stack_layers("7b", k=128, bits=4, g=128, dtype="f16", n_blocks=args.blocks)
-    stack = LinearStack(layers, n_cols=n)
+    # q/k/v and gate/up read the same x: one launch each (qeft_gemv_multi), 4 launches per block
+    groups = None if args.no_fuse else llama_launch_groups(args.blocks)
+    stack = LinearStack(layers, n_cols=n, groups=groups)
+    launches = stack.launches_per_step()
     for _ in range(args.warmup):
         stack.step()
     bytes_step = stack.bytes_per_step()
@@ -301,7 +304,9 @@ def run_b200(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
             "data": "synthetic",
             "config": {"workload": workload(args.blocks, n), "n_cols": n, "blocks": args.blocks,
-                       "gemv_per_step": n_layers, "bytes_per_step": bytes_step,
+                       "gemv_per_step": n_layers, "launches_per_step": launches,
+                       "fused_launches": "q/k/v and gate/up share x: one qeft_gemv_multi launch each" if groups else None,
+                       "bytes_per_step": bytes_step,
                        "l2": "inputs larger than L2 (%.2f GB of weights per step)" % (bytes_step / 1e9),
                        "parallelism": f"replicas{ws}"},
             "frac_of_peak": value / ws / peak, "peak_gbs": peak, "peak_kind": peak_kind,
@@ -311,7 +316,7 @@ def run_b200(args):
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                          "per_shape": roof},
             "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "gpu_launches": n_layers * args.steps,
+            "gpu_launches": launches * args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "finetune": ft,
@@ -465,6 +470,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ft", action="store_true", help="skip the fine-tune step measurement")
+    ap.add_argument("--no-fuse", action="store_true", help="one GEMV launch per layer (no q/k/v, gate/up grouping)")
     ap.add_argument("--ft-blocks", type=int, default=32)
     ap.add_argument("--ft-seq", type=int, default=2048)
     ap.add_argument("--ft-mb", type=int, default=1)

@@ -93,6 +93,13 @@ size_t qeft_gemv_workspace_bytes(const qeft_linear_t* layer, int n_cols);
 int qeft_gemv(const qeft_linear_t* layer, const void* x, int64_t ldx, void* y, int64_t ldy, int y_f32,
               int n_cols, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Several layers that read the same x in ONE launch (a decoder's q/k/v or gate/up): their
+ * rows are concatenated, each layer writes its own y (ys[l], common ldy). Up to 3 layers with
+ * identical ic, k, bits, g, act_dtype, flags (and column map). */
+int qeft_gemv_multi(const qeft_linear_t* const* layers, int n_layers, const void* x, int64_t ldx,
+                    void* const* ys, int64_t ldy, int y_f32, int n_cols, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
 /* ---- prefill / fine-tune GEMMs on tcgen05 (tuning.py:52-103) ----
  * fwd:   y[t][o]  = sum_i W_hat[o][i] x[t][i]                       (qlinear_forward_train)
  * dgrad: dx[t][i] = sum_o W_hat[o][i] dy[t][o]  (+= if accumulate)  (qlinear_backward dX)

@@ -57,16 +57,22 @@ int num_sms() {
   return n;
 }
 
+constexpr int kMaxLayers = 3;  // layers sharing x in one launch (q/k/v, gate/up)
+
 struct GemvArgs {
-  const uint8_t* qw;
-  const float2* sz;
-  const uint8_t* weak16;
+  // per layer (rows concatenated in launch order): codes, group params, weak tiles, output
+  const uint8_t* qw[kMaxLayers];
+  const float2* sz[kMaxLayers];
+  const uint8_t* weak16[kMaxLayers];
+  void* ys[kMaxLayers];
+  int ocs[kMaxLayers];
+  int rb_end[kMaxLayers];  // cumulative row-block counts
+  int nl;
   const uint8_t* x;  // fast: original columns; else pre-gathered B200 order [n][m_pad + k_pad]
   int64_t ldx;       // elements
-  void* y;
   int64_t ldy;
   int y_f32;
-  int oc, m, m_pad, k, k_pad, g, ng, n, n_rb;
+  int m, m_pad, k, k_pad, g, ng, n, n_rb;
   int gathered;
   int nsq;      // quantized 64-column steps (m_pad / 64)
   int spw;      // quantized steps per warp (multiple of the group's steps)
@@ -76,11 +82,19 @@ struct GemvArgs {
 };
 
 template <typename T>
-__device__ __forceinline__ void store_out(const GemvArgs& a, int n, int row, float v) {
+__device__ __forceinline__ void store_out(const GemvArgs& a, void* y, int n, int row, float v) {
   if (a.y_f32)
-    ((float*)a.y)[(int64_t)n * a.ldy + row] = v;
+    ((float*)y)[(int64_t)n * a.ldy + row] = v;
   else
-    ((T*)a.y)[(int64_t)n * a.ldy + row] = from_f32<T>(v);
+    ((T*)y)[(int64_t)n * a.ldy + row] = from_f32<T>(v);
+}
+
+// global row-block -> (layer, layer-local row-block)
+QEFT_DEV int layer_of(const GemvArgs& a, int grb, int& rb) {
+  int l = 0;
+  while (l + 1 < a.nl && grb >= a.rb_end[l]) ++l;
+  rb = grb - (l ? a.rb_end[l - 1] : 0);
+  return l;
 }
 
 QEFT_DEV uint4 ldg_l1(const void* p) {
@@ -197,7 +211,9 @@ gemv_kernel(const GemvArgs a) {
     using T2 = typename DTraits<T>::T2;
     const float2 cf = t2_to_f2<T2>(magic_to_code<T>(mag, hi16));
     const int gA = min(col / a.g, a.ng - 1), gB = min((col + 1) / a.g, a.ng - 1);
-    const float2* sz = a.sz + (int64_t)rb * a.ng * 16;
+    int lrb;
+    const int l = layer_of(a, rb, lrb);
+    const float2* sz = a.sz[l] + (int64_t)lrb * a.ng * 16;
     const float2 pA = sz[gA * 16 + row_local];
     const float2 pB = sz[gB * 16 + row_local];
     T2 r;
@@ -297,9 +313,10 @@ gemv_kernel(const GemvArgs a) {
   auto issue_next = [&](int t) {
     if (t < TB && !a.dbg) {
       uint8_t* slot = ring + (t % kR) * kSlot;
-      const int rb = rb_of(ij);
+      int rb;
+      const int l = layer_of(a, rb_of(ij), rb);
       const int b0 = s_beg + ib * kU;
-      const uint8_t* base = a.qw + rb * a.rbb;
+      const uint8_t* base = a.qw[l] + rb * a.rbb;
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int st = b0 + u;
@@ -315,7 +332,7 @@ gemv_kernel(const GemvArgs a) {
         }
       }
       if (FOLD && lane < 16) {
-        const float2* szp = a.sz + ((int64_t)rb * a.ng) * 16 + lane;
+        const float2* szp = a.sz[l] + ((int64_t)rb * a.ng) * 16 + lane;
 #pragma unroll
         for (int i = 0; i < kSP; ++i) {
           if (b0 + i * G < s_end) {
@@ -441,7 +458,9 @@ gemv_kernel(const GemvArgs a) {
   auto issue_weak = [&](int j) {
     if (nwt > 0 && j < nrbc) {
       mbar_expect_tx(&wbar[j & 1], wbytes);
-      bulk_g2s(wsm + (j & 1) * wbytes, a.weak16 + (int64_t)rb_of(j) * wbytes, wbytes, &wbar[j & 1]);
+      int rb;
+      const int l = layer_of(a, rb_of(j), rb);
+      bulk_g2s(wsm + (j & 1) * wbytes, a.weak16[l] + (int64_t)rb * wbytes, wbytes, &wbar[j & 1]);
     }
   };
   if (threadIdx.x == 0) {
@@ -536,8 +555,10 @@ gemv_kernel(const GemvArgs a) {
       float v = 0.f;
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) v += pp[w][rl][n];
-      const int row = rb * 16 + rl;
-      if (row < a.oc) store_out<T>(a, n, row, v);
+      int lrb;
+      const int l = layer_of(a, rb, lrb);
+      const int row = lrb * 16 + rl;
+      if (row < a.ocs[l]) store_out<T>(a, a.ys[l], n, row, v);
     }
   };
 
@@ -613,21 +634,36 @@ size_t gemv_workspace_bytes(const qeft_linear_t* L, int n) {
   return (size_t)n * (L->m_pad + L->k_pad) * 2 + 256;
 }
 
-int gemv(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ldy, int y_f32, int n,
-         void* ws, size_t ws_bytes, cudaStream_t st) {
+int gemv_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ldx, void* const* ys, int64_t ldy,
+               int y_f32, int n, void* ws, size_t ws_bytes, cudaStream_t st) {
+  QEFT_CHECK(nl >= 1 && nl <= kMaxLayers, QEFT_ERR_SHAPE, "gemv: %d layers per launch (1..%d)", nl, kMaxLayers);
+  const qeft_linear_t* L = Ls[0];
   QEFT_CHECK(n >= 1 && n <= 16, QEFT_ERR_SHAPE, "gemv: n_cols=%d outside 1..16", n);
   QEFT_CHECK(L->bits == 3 || L->bits == 4, QEFT_ERR_SHAPE, "gemv: bits=%d", L->bits);
-  QEFT_CHECK(ldx >= L->ic && ldy >= L->oc, QEFT_ERR_SHAPE, "gemv: ld too small");
   GemvArgs a{};
-  a.qw = (const uint8_t*)L->qweight;
-  a.sz = (const float2*)L->sz;
-  a.weak16 = (const uint8_t*)L->weak16;
-  a.y = y;
+  a.nl = nl;
+  int rb_total = 0;
+  for (int l = 0; l < nl; ++l) {
+    const qeft_linear_t* Li = Ls[l];
+    // layers of one launch share x: identical K geometry, dtype and column map
+    QEFT_CHECK(Li->ic == L->ic && Li->k == L->k && Li->bits == L->bits && Li->g == L->g &&
+                   Li->act_dtype == L->act_dtype && Li->flags == L->flags &&
+                   (Li->colmap == L->colmap || (L->flags & QEFT_FLAG_STRUCTURED_FAST)),
+               QEFT_ERR_SHAPE, "gemv: layer %d does not share the first layer's input geometry", l);
+    QEFT_CHECK(ldx >= Li->ic && ldy >= Li->oc, QEFT_ERR_SHAPE, "gemv: ld too small");
+    a.qw[l] = (const uint8_t*)Li->qweight;
+    a.sz[l] = (const float2*)Li->sz;
+    a.weak16[l] = (const uint8_t*)Li->weak16;
+    a.ys[l] = ys[l];
+    a.ocs[l] = Li->oc;
+    rb_total += Li->oc_pad / 16;
+    a.rb_end[l] = rb_total;
+  }
   a.ldy = ldy;
   a.y_f32 = y_f32;
-  a.oc = L->oc; a.m = L->m; a.m_pad = L->m_pad; a.k = L->k; a.k_pad = L->k_pad;
+  a.m = L->m; a.m_pad = L->m_pad; a.k = L->k; a.k_pad = L->k_pad;
   a.g = L->g; a.ng = L->ng; a.n = n;
-  a.n_rb = L->oc_pad / 16;
+  a.n_rb = rb_total;
   a.rbb = rowblock_bytes(L->bits, L->m_pad);
   a.nsq = L->m_pad / 64;
   a.dbg = env_int("QEFT_GEMV_DEBUG", 0);
@@ -657,6 +693,11 @@ int gemv(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ld
   const bool bf = L->act_dtype == QEFT_BF16;
   if (L->bits == 4) return bf ? dispatch_gt<4, __nv_bfloat16>(a, gt, st) : dispatch_gt<4, __half>(a, gt, st);
   return bf ? dispatch_gt<3, __nv_bfloat16>(a, gt, st) : dispatch_gt<3, __half>(a, gt, st);
+}
+
+int gemv(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ldy, int y_f32, int n,
+         void* ws, size_t ws_bytes, cudaStream_t st) {
+  return gemv_multi(&L, 1, x, ldx, &y, ldy, y_f32, n, ws, ws_bytes, st);
 }
 
 }  // namespace qeft

@@ -44,6 +44,8 @@ int quantize_rtn(const float* w, int oc, int m, int g, int bits, float* s, float
 size_t gemv_workspace_bytes(const qeft_linear_t* L, int n);
 int gemv(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ldy, int y_f32, int n,
          void* ws, size_t ws_bytes, cudaStream_t st);
+int gemv_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ldx, void* const* ys, int64_t ldy,
+               int y_f32, int n, void* ws, size_t ws_bytes, cudaStream_t st);
 
 size_t gemm_workspace_bytes(const qeft_linear_t* L, int T);
 int gemm_fwd(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ldy, int T,

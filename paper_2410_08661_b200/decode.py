@@ -12,10 +12,13 @@ reference's per-token loop in `bench_generate`, pkg/src/qeft/kernels.py:
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 
 from . import _lib
-from .layer import DeviceLayer, _pad, torch_dtype
+from .errors import ShapeError
+from .layer import WORKSPACE, DeviceLayer, _pad, torch_dtype
 
 LLAMA_SHAPES = {
     # name -> (oc, ic) for one decoder block
@@ -59,6 +62,36 @@ def random_layer(oc, ic, k=128, bits=4, g=128, dtype="f16", seed=0, device="cuda
                        structured_fast=(m % 8 == 0 and ic % 8 == 0))
 
 
+def gemv_multi(layers, x, outs):
+    """One decode-GEMV launch over layers that read the same x (qeft_gemv_multi): a
+    decoder's q/k/v or gate/up. outs[l] is layer l's (n, oc_l) output."""
+    n = x.shape[0]
+    L = _lib.lib()
+    arr = (ctypes.POINTER(_lib.QeftLinearT) * len(layers))(*[l.cptr for l in layers])
+    ys = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+    ldy = outs[0].stride(0) if n > 1 else max(l.oc for l in layers)
+    if any((o.stride(0) if n > 1 else ldy) != ldy for o in outs):
+        raise ShapeError("gemv_multi: outputs need a common row stride")
+    wsb = max(int(L.qeft_gemv_workspace_bytes(l.cptr, n)) for l in layers)
+    ws = WORKSPACE.get(wsb, x.device)
+    ldx = x.stride(0) if n > 1 else layers[0].ic
+    _lib.check(L.qeft_gemv_multi(ctypes.cast(arr, ctypes.c_void_p), len(layers), _lib.ptr(x), ldx,
+                                 ctypes.cast(ys, ctypes.c_void_p), ldy,
+                                 1 if outs[0].dtype.itemsize == 4 else 0, n, _lib.ptr(ws), ws.numel(),
+                                 _lib.stream_ptr()), "gemv_multi")
+    return outs
+
+
+def llama_launch_groups(n_blocks):
+    """Layers of one decode launch per block of llama_stack_layers' order (wq, wk, wv, wo,
+    w_up, w_gate, w_down): q/k/v share x, so do gate/up."""
+    groups = []
+    for b in range(n_blocks):
+        i = 7 * b
+        groups += [[i, i + 1, i + 2], [i + 3], [i + 4, i + 5], [i + 6]]
+    return groups
+
+
 def llama_stack_layers(model="7b", k=128, bits=4, g=128, dtype="f16", n_blocks=None, seed=0):
     layers = []
     for b in range(n_blocks if n_blocks is not None else N_BLOCKS[model]):
@@ -70,10 +103,12 @@ def llama_stack_layers(model="7b", k=128, bits=4, g=128, dtype="f16", n_blocks=N
 class LinearStack:
     """Run every layer's GEMV once per step (decode of one token batch)."""
 
-    def __init__(self, layers, n_cols=1, use_graph=True):
+    def __init__(self, layers, n_cols=1, use_graph=True, groups=None):
         import torch
         self.layers = layers
         self.n = n_cols
+        # launch groups: layers sharing x in one qeft_gemv_multi launch (default: one per layer)
+        self.groups = groups if groups is not None else [[i] for i in range(len(layers))]
         dev = layers[0].device
         td = layers[0].tdtype
         self.ics = sorted({l.ic for l in layers})
@@ -99,8 +134,13 @@ class LinearStack:
             self.graph = g
 
     def _launch(self):
-        for l, y in zip(self.layers, self.y):
-            l.gemv(self.x[l.ic], out=y)
+        for grp in self.groups:
+            if len(grp) == 1:
+                l = self.layers[grp[0]]
+                l.gemv(self.x[l.ic], out=self.y[grp[0]])
+            else:
+                gemv_multi([self.layers[i] for i in grp], self.x[self.layers[grp[0]].ic],
+                           [self.y[i] for i in grp])
 
     def step(self):
         if self.graph is not None:
@@ -109,7 +149,7 @@ class LinearStack:
             self._launch()
 
     def launches_per_step(self) -> int:
-        return len(self.layers)
+        return len(self.groups)
 
     def bytes_per_step(self) -> int:
         """Algorithmic HBM bytes (weights + fp16 x and y)."""
