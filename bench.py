@@ -191,23 +191,35 @@ def _time_graph(fn, iters, torch):
     return e0.elapsed_time(e1) / 1e3
 
 
-def kernel_roofline(torch, n_blocks, peak, n_cols):
-    """Per-shape GEMV launch time (CUDA events on the launching stream, graph of the
-    32 same-shape layers so weights stream from HBM). Returns per-shape table."""
+# launch types of one decoder block: (name, layers in the launch as (oc, ic), launches per block)
+LAUNCHES = [("qkv", [(4096, 4096)] * 3, 1), ("o", [(4096, 4096)], 1),
+            ("gate_up", [(11008, 4096)] * 2, 1), ("down", [(4096, 11008)], 1)]
+
+
+def kernel_roofline(torch, n_blocks, peak, n_cols, fuse=True):
+    """Per-launch GEMV time of each launch type of the stack (CUDA events on the launching
+    stream; a graph of n_blocks launches of that type, distinct weights, so they stream
+    from HBM). Returns the per-launch table."""
     from paper_2410_08661_b200.decode import LinearStack, random_layer
     out = []
-    for si, (oc, ic) in enumerate(sorted(set(BLOCK_SHAPES))):
-        layers = [random_layer(oc, ic, 128, 4, 128, "f16", seed=9000 + si * 100 + b)
-                  for b in range(n_blocks)]
-        st = LinearStack(layers, n_cols=n_cols)
+    for si, (name, shapes, _) in enumerate(LAUNCHES):
+        if not fuse and len(shapes) > 1:
+            shapes = shapes[:1]
+        layers, groups = [], []
+        for b in range(n_blocks):
+            groups.append(list(range(len(layers), len(layers) + len(shapes))))
+            layers += [random_layer(oc, ic, 128, 4, 128, "f16", seed=9000 + si * 100 + b * 3 + i)
+                       for i, (oc, ic) in enumerate(shapes)]
+        st = LinearStack(layers, n_cols=n_cols, groups=groups)
         for _ in range(3):
             st.step()
         reps = 20
         t = _time_graph(st.step, reps, torch)
-        per_launch = t / (reps * len(layers))
-        nb = st.bytes_per_step() / len(layers)
-        out.append({"shape": [oc, ic], "us_per_launch": per_launch * 1e6, "bytes_per_launch": nb,
-                    "achieved_gbs": nb / per_launch / 1e9, "frac": nb / per_launch / 1e9 / peak})
+        per_launch = t / (reps * n_blocks)
+        nb = st.bytes_per_step() / n_blocks
+        out.append({"launch": name, "shapes": [list(x) for x in shapes], "us_per_launch": per_launch * 1e6,
+                    "bytes_per_launch": nb, "achieved_gbs": nb / per_launch / 1e9,
+                    "frac": nb / per_launch / 1e9 / peak})
         del st, layers
     return out
 
@@ -280,20 +292,19 @@ def run_b200(args):
         te = float(tt.item())
     e2e = ws * bytes_step * args.steps / te / 1e9
 
-    roof = kernel_roofline(torch, min(args.blocks, 32), peak, n) if rank == 0 else []
+    roof = kernel_roofline(torch, min(args.blocks, 32), peak, n, fuse=not args.no_fuse) if rank == 0 else []
     n_layers = len(layers)
     del stack, layers
     torch.cuda.empty_cache()
     ft = None if args.no_ft else finetune_bench(args, ws, rank, dev, torch)
     line = None
     if rank == 0:
-        count = {(4096, 4096): 4, (11008, 4096): 2, (4096, 11008): 1}
-        dom = max(roof, key=lambda r: r["us_per_launch"] * count[tuple(r["shape"])])
+        dom = max(roof, key=lambda r: r["us_per_launch"])  # one launch of each type per block
         traffic = None
         import glob
         tps = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "gemv_traffic.json")))
         if tps:  # dram__bytes_read + write per launch from the latest committed ncu capture
-            traffic = json.load(open(tps[-1])).get("%dx%d" % tuple(dom["shape"]))
+            traffic = json.load(open(tps[-1])).get(dom["launch"])
         cpu = None
         if ws == 1 and not args.no_cpu:
             gbs, sample, cores = cpu_oracle_sample(seconds=args.cpu_seconds)
@@ -312,7 +323,8 @@ def run_b200(args):
             "frac_of_peak": value / ws / peak, "peak_gbs": peak, "peak_kind": peak_kind,
             "roofline": {"bound": "hbm", "achieved": dom["achieved_gbs"], "peak": peak,
                          "unit": "GB/s", "frac": dom["frac"], "traffic": traffic,
-                         "kernel": "gemv_kernel<4-bit, N=1, g=128, fp16> %dx%d (largest share of the step)" % tuple(dom["shape"]),
+                         "kernel": "gemv_kernel<4-bit, N=%d, g=128, fp16> launch %s %s (largest share of the step)"
+                                   % (n, dom["launch"], dom["shapes"]),
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                          "per_shape": roof},
             "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
