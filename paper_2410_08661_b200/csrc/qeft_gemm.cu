@@ -176,7 +176,7 @@ QEFT_DEV void dequant_lane_general(const uint32_t* words, uint32_t hb, const flo
 template <int MODE, int BITS, typename T, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ CUtensorMap map_b1,
-            const GemmArgs a) {
+            const __grid_constant__ CUtensorMap map_w, const GemmArgs a) {
   constexpr int kStageB = BN * BK * 2;
   constexpr int kStages = (BN == 256) ? 4 : 6;
   constexpr int kTmemCols = 2 * BN;
@@ -204,6 +204,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     fence_mbar_init();
     tc::prefetch_tmap(&map_b0);
     tc::prefetch_tmap(&map_b1);
+    if (a.k) tc::prefetch_tmap(&map_w);
   }
   if (warp == 1) tc::tmem_alloc(&tmem_base, kTmemCols);
   tc::fence_before();
@@ -219,12 +220,27 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     if (lane == 0) {
       int it = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int n_blk = tile / a.n_mblk;
+        const int n_blk = tile / a.n_mblk, m_blk = tile % a.n_mblk;
         const int tok0 = n_blk * BN;
         for (int kb = 0; kb < a.n_kblk; ++kb, ++it) {
           const int s = it % kStages;
           mbar_wait(&empty_bar[s], ((it / kStages) & 1) ^ 1);
-          mbar_expect_tx(&full_bar[s], kStageB);
+          // the weak block is already fp16/bf16 in 16 x 64 row-block tiles: TMA places it in
+          // the A stage (SWIZZLE_128B, the layout the dequant producers write)
+          uint32_t wbytes = 0;
+          if (MODE == MODE_FWD && kb >= a.kq) wbytes = kStageA;
+          if (MODE == MODE_DGRAD && m_blk >= a.kq)
+            wbytes = (((m_blk - a.kq) * 2 + 1) * 64 < a.k_pad) ? kStageA : kStageA / 2;
+          mbar_expect_tx(&full_bar[s], kStageB + wbytes);
+          if (MODE == MODE_FWD && kb >= a.kq) {
+            tc::tma_load_4d(sA + s * kStageA, &map_w, 0, 0, kb - a.kq, 8 * m_blk, &full_bar[s]);
+          } else if (MODE == MODE_DGRAD && m_blk >= a.kq) {
+            // MN-major A: two 64-row halves, one per weak K-tile (the second may be past k_pad)
+            const int kw0 = (m_blk - a.kq) * 2;
+            tc::tma_load_4d(sA + s * kStageA, &map_w, 0, 0, kw0, 4 * kb, &full_bar[s]);
+            if (wbytes == kStageA)
+              tc::tma_load_4d(sA + s * kStageA + 8192, &map_w, 0, 0, kw0 + 1, 4 * kb, &full_bar[s]);
+          }
           if (MODE == MODE_FWD && !a.gathered && kb >= a.kq)
             tc::tma_load_2d(sB + s * kStageB, &map_b1, (kb - a.kq) * BK, tok0, &full_bar[s]);
           else
@@ -271,8 +287,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     const int pw = warp - 2;
     const int g8 = lane >> 2, t4 = lane & 3;
     const bool fold16 = (a.g % 16) == 0;
+    // weak tiles arrive by TMA (already fp16/bf16), so a unit in flight is 16 B of codes + params
     struct Pre {
-      uint4 v[kUPW][4];   // quant: v[h][0] = lane codes (3-bit: .x,.y = 2-bit words, .z = hi word); weak: 64 B
+      uint4 v[kUPW];  // lane codes of unit h (3-bit: .x,.y = 2-bit words, .z = hi word)
       float2 p0[kUPW], p1[kUPW];
     };
     // unit geometry: row-block, 64-column tile index in the B200 order, weak tile (or -1)
@@ -294,27 +311,20 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
         int rb, jt, kw;
         unit(m_blk, kb, h, rb, jt, kw);
         if (rb * 16 >= a.oc || (kw >= 0 && kw * 64 >= a.k_pad)) continue;
-        if (kw < 0) {
-          if constexpr (BITS == 4) {
-            P.v[h][0] = ldg_stream(a.qw + ((int64_t)rb * (a.m_pad >> 6) + jt) * 512 + lane * 16);
-          } else {
-            const uint8_t* tb = a.qw + ((int64_t)rb * (a.m_pad >> 7) + (jt >> 1)) * 768;
-            const uint2 w2 = *reinterpret_cast<const uint2*>(tb + lane * 16 + 8 * (jt & 1));
-            P.v[h][0] = make_uint4(w2.x, w2.y, *reinterpret_cast<const uint32_t*>(tb + 512 + lane * 8 + 4 * (jt & 1)), 0u);
-          }
-          if (fold16) {
-            const float2* szr = a.sz + (int64_t)rb * a.ng * 16;
-            const int col = jt * BK + 16 * t4;
-            const int gi = min(a.g_shift >= 0 ? (col >> a.g_shift) : col / a.g, a.ng - 1);
-            P.p0[h] = szr[gi * 16 + g8];
-            P.p1[h] = szr[gi * 16 + g8 + 8];
-          }
+        if (kw >= 0 || rb * 16 >= a.oc) continue;  // weak tiles arrive by TMA
+        if constexpr (BITS == 4) {
+          P.v[h] = ldg_stream(a.qw + ((int64_t)rb * (a.m_pad >> 6) + jt) * 512 + lane * 16);
         } else {
-          const T* wt = (const T*)a.weak16 + ((int64_t)rb * (a.k_pad >> 6) + kw) * 1024;
-          P.v[h][0] = *reinterpret_cast<const uint4*>(wt + g8 * 64 + 16 * t4);
-          P.v[h][1] = *reinterpret_cast<const uint4*>(wt + g8 * 64 + 16 * t4 + 8);
-          P.v[h][2] = *reinterpret_cast<const uint4*>(wt + (g8 + 8) * 64 + 16 * t4);
-          P.v[h][3] = *reinterpret_cast<const uint4*>(wt + (g8 + 8) * 64 + 16 * t4 + 8);
+          const uint8_t* tb = a.qw + ((int64_t)rb * (a.m_pad >> 7) + (jt >> 1)) * 768;
+          const uint2 w2 = *reinterpret_cast<const uint2*>(tb + lane * 16 + 8 * (jt & 1));
+          P.v[h] = make_uint4(w2.x, w2.y, *reinterpret_cast<const uint32_t*>(tb + 512 + lane * 8 + 4 * (jt & 1)), 0u);
+        }
+        if (fold16) {
+          const float2* szr = a.sz + (int64_t)rb * a.ng * 16;
+          const int col = jt * BK + 16 * t4;
+          const int gi = min(a.g_shift >= 0 ? (col >> a.g_shift) : col / a.g, a.ng - 1);
+          P.p0[h] = szr[gi * 16 + g8];
+          P.p1[h] = szr[gi * 16 + g8 + 8];
         }
       }
     };
@@ -323,24 +333,19 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       for (int h = 0; h < kUPW; ++h) {
         int rb, jt, kw;
         unit(m_blk, kb, h, rb, jt, kw);
+        if (kw >= 0 && kw * 64 < a.k_pad) continue;  // written by the TMA warp
         uint32_t out[16];
-        if (rb * 16 >= a.oc || (kw >= 0 && kw * 64 >= a.k_pad)) {
+        if (rb * 16 >= a.oc || kw >= 0) {
 #pragma unroll
           for (int e = 0; e < 16; ++e) out[e] = 0u;
-        } else if (kw < 0) {
-          const uint32_t words[4] = {P.v[h][0].x, P.v[h][0].y, P.v[h][0].z, P.v[h][0].w};
-          const uint32_t hb = (BITS == 3) ? P.v[h][0].z : 0u;
+        } else {
+          const uint32_t words[4] = {P.v[h].x, P.v[h].y, P.v[h].z, P.v[h].w};
+          const uint32_t hb = (BITS == 3) ? P.v[h].z : 0u;
           if (fold16) {
             dequant_lane_packed<BITS, T>(words, hb, P.p0[h], P.p1[h], out);
           } else {
             const float2* szr = a.sz + (int64_t)rb * a.ng * 16;
             dequant_lane_general<BITS, T>(words, hb, szr + g8, szr + g8 + 8, jt * BK + 16 * t4, a.g, a.ng, out);
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            out[4 * q] = P.v[h][q].x; out[4 * q + 1] = P.v[h][q].y;
-            out[4 * q + 2] = P.v[h][q].z; out[4 * q + 3] = P.v[h][q].w;
           }
         }
         uint32_t o0, o1, o2, o3;  // byte offsets of (row g, chunk 2t), (g, 2t+1), (g+8, 2t), (g+8, 2t+1)
@@ -644,6 +649,23 @@ int make_map(CUtensorMap* m, const void* base, int dtype, int64_t inner, int64_t
   return 0;
 }
 
+// weak16 [oc_pad/16][k_pad/64][16][64] as a 4-D tensor, box {64, 16, 1, box_rb}, SWIZZLE_128B
+int make_weak_map(CUtensorMap* m, const void* weak16, int dtype, int k_pad, int n_rb, int box_rb) {
+  auto fn = encode_fn();
+  QEFT_CHECK(fn != nullptr, QEFT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  QEFT_CHECK(((uintptr_t)weak16 & 15) == 0, QEFT_ERR_LAYOUT, "weak16 must be 16-byte aligned");
+  cuuint64_t dims[4] = {64, 16, (cuuint64_t)(k_pad / 64), (cuuint64_t)n_rb};
+  cuuint64_t strides[3] = {128, 2048, (cuuint64_t)(k_pad / 64) * 2048};
+  cuuint32_t box[4] = {64, 16, 1, (cuuint32_t)box_rb};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, dtype == QEFT_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                  const_cast<void*>(weak16), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  QEFT_CHECK(r == CUDA_SUCCESS, QEFT_ERR_CUDA, "cuTensorMapEncodeTiled (weak) failed (%d)", (int)r);
+  return 0;
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -656,7 +678,8 @@ int num_sms() {
 }
 
 template <int MODE, int BITS, typename T, int BN>
-int launch_gemm(const CUtensorMap& m0, const CUtensorMap& m1, const GemmArgs& a, cudaStream_t st) {
+int launch_gemm(const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& mw, const GemmArgs& a,
+                cudaStream_t st) {
   constexpr int kStageB = BN * BK * 2;
   constexpr int kStages = (BN == 256) ? 4 : 6;
   const size_t smem = 1024 + (size_t)kStages * (kStageA + kStageB) + (size_t)kEpiWarps * 32 * kEpiStride * 2;
@@ -668,19 +691,27 @@ int launch_gemm(const CUtensorMap& m0, const CUtensorMap& m1, const GemmArgs& a,
   }
   const int tiles = a.n_mblk * a.n_nblk;
   const int grid = std::min(tiles, num_sms());
-  QEFT_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, m0, m1, a));
+  QEFT_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, m0, m1, mw, a));
   return 0;
 }
 
 template <int MODE, typename T>
-int dispatch_gemm(int bits, int T_, const CUtensorMap& m0, const CUtensorMap& m1, GemmArgs& a,
+int dispatch_gemm(const qeft_linear_t* L, int T_, const CUtensorMap& m0, const CUtensorMap& m1, GemmArgs& a,
                   cudaStream_t st) {
   const bool big = T_ > 128;
   const int BN = big ? 256 : 128;
   a.n_nblk = (T_ + BN - 1) / BN;
-  if (bits == 4)
-    return big ? launch_gemm<MODE, 4, T, 256>(m0, m1, a, st) : launch_gemm<MODE, 4, T, 128>(m0, m1, a, st);
-  return big ? launch_gemm<MODE, 3, T, 256>(m0, m1, a, st) : launch_gemm<MODE, 3, T, 128>(m0, m1, a, st);
+  // weak block as a 4-D tensor {64 columns, 16 rows, k_pad/64 tiles, row-blocks} of the
+  // row-block tile layout (weak_off, qeft_common.cuh); box = 8 row-blocks (fwd: the 128 rows of
+  // the K-major A tile) or 4 row-blocks (dgrad: one 64-row half of the MN-major A tile)
+  CUtensorMap mw = m0;
+  if (L->k) {
+    if (int r = make_weak_map(&mw, L->weak16, L->act_dtype, L->k_pad, L->oc_pad / 16, MODE == MODE_FWD ? 8 : 4))
+      return r;
+  }
+  if (L->bits == 4)
+    return big ? launch_gemm<MODE, 4, T, 256>(m0, m1, mw, a, st) : launch_gemm<MODE, 4, T, 128>(m0, m1, mw, a, st);
+  return big ? launch_gemm<MODE, 3, T, 256>(m0, m1, mw, a, st) : launch_gemm<MODE, 3, T, 128>(m0, m1, mw, a, st);
 }
 
 GemmArgs base_args(const qeft_linear_t* L, int T_) {
@@ -760,8 +791,8 @@ int gemm_fwd(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_
     m1 = m0;
     a.gathered = 1;
   }
-  if (L->act_dtype == QEFT_F16) return dispatch_gemm<MODE_FWD, __half>(L->bits, T_, m0, m1, a, st);
-  return dispatch_gemm<MODE_FWD, __nv_bfloat16>(L->bits, T_, m0, m1, a, st);
+  if (L->act_dtype == QEFT_F16) return dispatch_gemm<MODE_FWD, __half>(L, T_, m0, m1, a, st);
+  return dispatch_gemm<MODE_FWD, __nv_bfloat16>(L, T_, m0, m1, a, st);
 }
 
 int gemm_dgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, void* dx, int64_t lddx, int T_,
@@ -781,8 +812,8 @@ int gemm_dgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, void* dx, i
   CUtensorMap m0;
   const int box = T_ > 128 ? 256 : 128;
   if (int r = make_map(&m0, dy, L->act_dtype, L->oc, T_, lddy, box)) return r;
-  if (L->act_dtype == QEFT_F16) return dispatch_gemm<MODE_DGRAD, __half>(L->bits, T_, m0, m0, a, st);
-  return dispatch_gemm<MODE_DGRAD, __nv_bfloat16>(L->bits, T_, m0, m0, a, st);
+  if (L->act_dtype == QEFT_F16) return dispatch_gemm<MODE_DGRAD, __half>(L, T_, m0, m0, a, st);
+  return dispatch_gemm<MODE_DGRAD, __nv_bfloat16>(L, T_, m0, m0, a, st);
 }
 
 template <typename T, int NW>
