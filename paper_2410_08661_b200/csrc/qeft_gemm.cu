@@ -173,29 +173,49 @@ QEFT_DEV void dequant_lane_general(const uint32_t* words, uint32_t hb, const flo
   }
 }
 
-template <int MODE, int BITS, typename T, int BN>
+// Ring depths: A stages (16 KB, dequantized / weak TMA) and B stages (BN x 64 activations).
+// A tile of NSUB sub-tiles reuses each A stage for NSUB MMA groups (N = BN each), so the
+// producers dequantize once per NSUB * BN tokens.
+template <int BN, int NSUB>
+struct GemmShape {
+  static constexpr int kStageB = BN * BK * 2;
+  static constexpr int kStagesA = NSUB == 2 ? 3 : (BN == 256 ? 4 : 6);
+  static constexpr int kStagesB = NSUB == 2 ? 5 : kStagesA;
+  static constexpr size_t kSmem =
+      1024 + (size_t)kStagesA * kStageA + (size_t)kStagesB * kStageB + (size_t)kEpiWarps * 32 * kEpiStride * 2;
+};
+
+template <int MODE, int BITS, typename T, int BN, int NSUB>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ CUtensorMap map_b1,
             const __grid_constant__ CUtensorMap map_w, const GemmArgs a) {
-  constexpr int kStageB = BN * BK * 2;
-  constexpr int kStages = (BN == 256) ? 4 : 6;
+  using Sh = GemmShape<BN, NSUB>;
+  constexpr int kStageB = Sh::kStageB;
+  constexpr int kStagesA = Sh::kStagesA, kStagesB = Sh::kStagesB;
+  // two accumulator slots of BN columns: sub-tile q (running count) uses slot q & 1
   constexpr int kTmemCols = 2 * BN;
+  constexpr int kTileN = BN * NSUB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned base for SWIZZLE_128B atoms
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + kStages * kStageA;
-  T* sE = reinterpret_cast<T*>(sB + kStages * kStageB);  // epilogue staging [4 warps][32][kEpiStride]
-  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], tfull_bar[2], tempty_bar[2];
+  uint8_t* sB = smem + kStagesA * kStageA;
+  T* sE = reinterpret_cast<T*>(sB + kStagesB * kStageB);  // epilogue staging [4 warps][32][kEpiStride]
+  __shared__ __align__(8) uint64_t fullA[kStagesA], emptyA[kStagesA], fullB[kStagesB], emptyB[kStagesB];
+  __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = a.n_mblk * a.n_nblk;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full_bar[s], 1 + kProdWarps);
-      mbar_init(&empty_bar[s], 1);
+    for (int s = 0; s < kStagesA; ++s) {
+      mbar_init(&fullA[s], 1 + kProdWarps);  // TMA warp (weak bytes, maybe 0) + producers
+      mbar_init(&emptyA[s], 1);
+    }
+    for (int s = 0; s < kStagesB; ++s) {
+      mbar_init(&fullB[s], 1);
+      mbar_init(&emptyB[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
@@ -218,33 +238,40 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
   if (warp == 0) {
     // ================= TMA producer: activation tiles =================
     if (lane == 0) {
-      int it = 0;
+      int it = 0, ib = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int n_blk = tile / a.n_mblk, m_blk = tile % a.n_mblk;
-        const int tok0 = n_blk * BN;
+        const int tok0 = n_blk * kTileN;
         for (int kb = 0; kb < a.n_kblk; ++kb, ++it) {
-          const int s = it % kStages;
-          mbar_wait(&empty_bar[s], ((it / kStages) & 1) ^ 1);
+          const int s = it % kStagesA;
+          mbar_wait(&emptyA[s], ((it / kStagesA) & 1) ^ 1);
           // the weak block is already fp16/bf16 in 16 x 64 row-block tiles: TMA places it in
           // the A stage (SWIZZLE_128B, the layout the dequant producers write)
           uint32_t wbytes = 0;
           if (MODE == MODE_FWD && kb >= a.kq) wbytes = kStageA;
           if (MODE == MODE_DGRAD && m_blk >= a.kq)
             wbytes = (((m_blk - a.kq) * 2 + 1) * 64 < a.k_pad) ? kStageA : kStageA / 2;
-          mbar_expect_tx(&full_bar[s], kStageB + wbytes);
+          mbar_expect_tx(&fullA[s], wbytes);
           if (MODE == MODE_FWD && kb >= a.kq) {
-            tc::tma_load_4d(sA + s * kStageA, &map_w, 0, 0, kb - a.kq, 8 * m_blk, &full_bar[s]);
+            tc::tma_load_4d(sA + s * kStageA, &map_w, 0, 0, kb - a.kq, 8 * m_blk, &fullA[s]);
           } else if (MODE == MODE_DGRAD && m_blk >= a.kq) {
             // MN-major A: two 64-row halves, one per weak K-tile (the second may be past k_pad)
             const int kw0 = (m_blk - a.kq) * 2;
-            tc::tma_load_4d(sA + s * kStageA, &map_w, 0, 0, kw0, 4 * kb, &full_bar[s]);
+            tc::tma_load_4d(sA + s * kStageA, &map_w, 0, 0, kw0, 4 * kb, &fullA[s]);
             if (wbytes == kStageA)
-              tc::tma_load_4d(sA + s * kStageA + 8192, &map_w, 0, 0, kw0 + 1, 4 * kb, &full_bar[s]);
+              tc::tma_load_4d(sA + s * kStageA + 8192, &map_w, 0, 0, kw0 + 1, 4 * kb, &fullA[s]);
           }
-          if (MODE == MODE_FWD && !a.gathered && kb >= a.kq)
-            tc::tma_load_2d(sB + s * kStageB, &map_b1, (kb - a.kq) * BK, tok0, &full_bar[s]);
-          else
-            tc::tma_load_2d(sB + s * kStageB, &map_b0, kb * BK, tok0, &full_bar[s]);
+#pragma unroll
+          for (int j = 0; j < NSUB; ++j, ++ib) {
+            const int sb = ib % kStagesB;
+            mbar_wait(&emptyB[sb], ((ib / kStagesB) & 1) ^ 1);
+            mbar_expect_tx(&fullB[sb], kStageB);
+            uint8_t* dst = sB + sb * kStageB;
+            if (MODE == MODE_FWD && !a.gathered && kb >= a.kq)
+              tc::tma_load_2d(dst, &map_b1, (kb - a.kq) * BK, tok0 + j * BN, &fullB[sb]);
+            else
+              tc::tma_load_2d(dst, &map_b0, kb * BK, tok0 + j * BN, &fullB[sb]);
+          }
         }
       }
     }
@@ -252,28 +279,38 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     // ================= MMA issuer (one thread) =================
     const uint32_t idesc = tc::idesc_f16(std::is_same<T, __nv_bfloat16>::value, BM, BN,
                                          MODE == MODE_DGRAD, false);
-    int it = 0, tcount = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
-      const int acc = tcount & 1;
-      mbar_wait(&tempty_bar[acc], ((tcount >> 1) & 1) ^ 1);
-      tc::fence_after();
-      const uint32_t d_tmem = tmem + acc * BN;
+    int it = 0, ib = 0, q0 = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, q0 += NSUB) {
       for (int kb = 0; kb < a.n_kblk; ++kb, ++it) {
-        const int s = it % kStages;
-        mbar_wait(&full_bar[s], (it / kStages) & 1);
+        const int s = it % kStagesA;
+        mbar_wait(&fullA[s], (it / kStagesA) & 1);
         tc::fence_after();
-        if (lane == 0) {
-          const uint32_t a0 = smem_u32(sA + s * kStageA), b0 = smem_u32(sB + s * kStageB);
+        const uint32_t a0 = smem_u32(sA + s * kStageA);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = (MODE == MODE_FWD) ? tc::smem_desc_sw128(a0 + 32 * k, 16, 1024)
-                                                   : tc::smem_desc_sw128(a0 + 2048 * k, 8192, 1024);
-            const uint64_t bd = tc::smem_desc_sw128(b0 + 32 * k, 16, 1024);
-            tc::mma_f16(d_tmem, ad, bd, idesc, (kb | k) ? 1u : 0u);
+        for (int j = 0; j < NSUB; ++j, ++ib) {
+          const int q = q0 + j, slot = q & 1;
+          if (kb == 0) {  // the epilogue has drained this slot's previous sub-tile
+            mbar_wait(&tempty_bar[slot], ((q >> 1) & 1) ^ 1);
+            tc::fence_after();
           }
-          tc::commit(&empty_bar[s]);
-          if (kb == a.n_kblk - 1) tc::commit(&tfull_bar[acc]);
+          const int sb = ib % kStagesB;
+          mbar_wait(&fullB[sb], (ib / kStagesB) & 1);
+          tc::fence_after();
+          if (lane == 0) {
+            const uint32_t b0 = smem_u32(sB + sb * kStageB);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t ad = (MODE == MODE_FWD) ? tc::smem_desc_sw128(a0 + 32 * k, 16, 1024)
+                                                     : tc::smem_desc_sw128(a0 + 2048 * k, 8192, 1024);
+              const uint64_t bd = tc::smem_desc_sw128(b0 + 32 * k, 16, 1024);
+              tc::mma_f16(tmem + slot * BN, ad, bd, idesc, (kb | k) ? 1u : 0u);
+            }
+            tc::commit(&emptyB[sb]);
+            if (kb == a.n_kblk - 1) tc::commit(&tfull_bar[slot]);
+          }
+          __syncwarp();
         }
+        if (lane == 0) tc::commit(&emptyA[s]);
         __syncwarp();
       }
     }
@@ -310,7 +347,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       for (int h = 0; h < kUPW; ++h) {
         int rb, jt, kw;
         unit(m_blk, kb, h, rb, jt, kw);
-        if (rb * 16 >= a.oc || (kw >= 0 && kw * 64 >= a.k_pad)) continue;
         if (kw >= 0 || rb * 16 >= a.oc) continue;  // weak tiles arrive by TMA
         if constexpr (BITS == 4) {
           P.v[h] = ldg_stream(a.qw + ((int64_t)rb * (a.m_pad >> 6) + jt) * 512 + lane * 16);
@@ -411,25 +447,26 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       }
       const int mb = cp.m_blk, kb = cp.kb;
       advance(cp);
-      const int s = it % kStages;
-      mbar_wait(&empty_bar[s], ((it / kStages) & 1) ^ 1);
+      const int s = it % kStagesA;
+      mbar_wait(&emptyA[s], ((it / kStagesA) & 1) ^ 1);
       process(mb, kb, P0, sA + s * kStageA);
       P0 = P1;
       P1 = P2;
       fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full_bar[s]);
+      if (lane == 0) mbar_arrive(&fullA[s]);
     }
   } else {
     // ================= epilogue: TMEM -> registers -> smem transpose -> global =================
     const int ew = warp - (2 + kProdWarps);
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     T* stg = sE + ew * 32 * kEpiStride;
-    int tcount = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
+    int q = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+    for (int j = 0; j < NSUB; ++j, ++q) {
       const int m_blk = tile % a.n_mblk, n_blk = tile / a.n_mblk;
-      const int acc = tcount & 1;
-      mbar_wait(&tfull_bar[acc], (tcount >> 1) & 1);
+      const int acc = q & 1;
+      mbar_wait(&tfull_bar[acc], (q >> 1) & 1);
       tc::fence_after();
       const int row_base = m_blk * BM + quad * 32;  // channel (fwd) / B200 column (dgrad) of lane 0
 #pragma unroll 1
@@ -441,7 +478,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
         for (int c = 0; c < 32; ++c) stg[c * kEpiStride + lane] = from_f32<T>(__uint_as_float(r[c]));
         __syncwarp();
         // thread = one token, 32 consecutive rows
-        const int tok = n_blk * BN + cb * 32 + lane;
+        const int tok = n_blk * kTileN + j * BN + cb * 32 + lane;
         if (tok < a.T) {
           const T* src = stg + lane * kEpiStride;
           if (MODE == MODE_FWD || a.fast_out) {
@@ -677,13 +714,12 @@ int num_sms() {
   return n;
 }
 
-template <int MODE, int BITS, typename T, int BN>
+template <int MODE, int BITS, typename T, int BN, int NSUB>
 int launch_gemm(const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& mw, const GemmArgs& a,
                 cudaStream_t st) {
-  constexpr int kStageB = BN * BK * 2;
-  constexpr int kStages = (BN == 256) ? 4 : 6;
-  const size_t smem = 1024 + (size_t)kStages * (kStageA + kStageB) + (size_t)kEpiWarps * 32 * kEpiStride * 2;
-  auto kern = gemm_kernel<MODE, BITS, T, BN>;
+  const size_t smem = GemmShape<BN, NSUB>::kSmem;
+  static_assert(GemmShape<BN, NSUB>::kSmem <= 227 * 1024, "GEMM smem");
+  auto kern = gemm_kernel<MODE, BITS, T, BN, NSUB>;
   static bool attr = false;
   if (!attr) {
     QEFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -698,9 +734,16 @@ int launch_gemm(const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap&
 template <int MODE, typename T>
 int dispatch_gemm(const qeft_linear_t* L, int T_, const CUtensorMap& m0, const CUtensorMap& m1, GemmArgs& a,
                   cudaStream_t st) {
+  // tile N: 128 tokens (T <= 128), 256, or 2 x 256 sharing each dequantized A stage (T > 256;
+  // QEFT_GEMM_NSUB=1 forces single sub-tiles)
+  static const int nsub_env = [] {
+    const char* e = getenv("QEFT_GEMM_NSUB");
+    return e ? atoi(e) : 0;
+  }();
   const bool big = T_ > 128;
+  const bool pair = T_ > 256 && nsub_env != 1;
   const int BN = big ? 256 : 128;
-  a.n_nblk = (T_ + BN - 1) / BN;
+  a.n_nblk = (T_ + BN * (pair ? 2 : 1) - 1) / (BN * (pair ? 2 : 1));
   // weak block as a 4-D tensor {64 columns, 16 rows, k_pad/64 tiles, row-blocks} of the
   // row-block tile layout (weak_off, qeft_common.cuh); box = 8 row-blocks (fwd: the 128 rows of
   // the K-major A tile) or 4 row-blocks (dgrad: one 64-row half of the MN-major A tile)
@@ -709,9 +752,12 @@ int dispatch_gemm(const qeft_linear_t* L, int T_, const CUtensorMap& m0, const C
     if (int r = make_weak_map(&mw, L->weak16, L->act_dtype, L->k_pad, L->oc_pad / 16, MODE == MODE_FWD ? 8 : 4))
       return r;
   }
-  if (L->bits == 4)
-    return big ? launch_gemm<MODE, 4, T, 256>(m0, m1, mw, a, st) : launch_gemm<MODE, 4, T, 128>(m0, m1, mw, a, st);
-  return big ? launch_gemm<MODE, 3, T, 256>(m0, m1, mw, a, st) : launch_gemm<MODE, 3, T, 128>(m0, m1, mw, a, st);
+  if (L->bits == 4) {
+    if (pair) return launch_gemm<MODE, 4, T, 256, 2>(m0, m1, mw, a, st);
+    return big ? launch_gemm<MODE, 4, T, 256, 1>(m0, m1, mw, a, st) : launch_gemm<MODE, 4, T, 128, 1>(m0, m1, mw, a, st);
+  }
+  if (pair) return launch_gemm<MODE, 3, T, 256, 2>(m0, m1, mw, a, st);
+  return big ? launch_gemm<MODE, 3, T, 256, 1>(m0, m1, mw, a, st) : launch_gemm<MODE, 3, T, 128, 1>(m0, m1, mw, a, st);
 }
 
 GemmArgs base_args(const qeft_linear_t* L, int T_) {

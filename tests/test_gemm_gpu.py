@@ -45,6 +45,10 @@ CASES = [
     (160, 512, 16, 4, 32, "bf16", 64, "irregular", False),
     (128, 384, 32, 4, 64, "bf16", 200, "structured", True),
     (96, 200, 8, 4, 40, "f16", 17, "structured", False),
+    # T > 256: two 256-token sub-tiles share each dequantized A stage (ragged last tile)
+    (256, 768, 64, 3, 128, "bf16", 700, "structured", False),
+    (160, 512, 16, 4, 32, "f16", 520, "irregular", False),
+    (128, 384, 32, 4, 64, "bf16", 1000, "structured", True),
 ]
 
 
