@@ -48,6 +48,7 @@ struct GemmArgs {
   int oc, m, m_pad, k, k_pad, g, ng;
   int T;
   int n_mblk, n_nblk, n_kblk, kq;  // kq: quantized k-blocks (fwd) / quantized m-tiles (dgrad)
+  int n_items, n_full;             // work items: [0, n_full) whole tiles, then half tiles (NSUB == 2)
   void* out;
   int64_t ldo;
   int accumulate;
@@ -206,7 +207,26 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
   __shared__ uint32_t tmem_base;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ntiles = a.n_mblk * a.n_nblk;
+  const int ntiles = a.n_items;
+  // work item -> (m-block, first token, sub-tiles). Items past n_full are the halves of the
+  // last partial wave's tiles, so that wave spreads over twice as many SMs.
+  struct Item {
+    int m_blk, tok0, nsub;
+  };
+  auto item = [&](int i) {
+    Item it;
+    int t = i, half = 0;
+    it.nsub = NSUB;
+    if (NSUB == 2 && i >= a.n_full) {
+      t = a.n_full + ((i - a.n_full) >> 1);
+      half = (i - a.n_full) & 1;
+      it.nsub = 1;
+    }
+    const int n_blk = t / a.n_mblk;
+    it.m_blk = t - n_blk * a.n_mblk;
+    it.tok0 = n_blk * kTileN + half * BN;
+    return it;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStagesA; ++s) {
@@ -240,8 +260,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     if (lane == 0) {
       int it = 0, ib = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int n_blk = tile / a.n_mblk, m_blk = tile % a.n_mblk;
-        const int tok0 = n_blk * kTileN;
+        const Item ti = item(tile);
+        const int m_blk = ti.m_blk, tok0 = ti.tok0;
         for (int kb = 0; kb < a.n_kblk; ++kb, ++it) {
           const int s = it % kStagesA;
           mbar_wait(&emptyA[s], ((it / kStagesA) & 1) ^ 1);
@@ -263,6 +283,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
           }
 #pragma unroll
           for (int j = 0; j < NSUB; ++j, ++ib) {
+            if (j >= ti.nsub) break;
             const int sb = ib % kStagesB;
             mbar_wait(&emptyB[sb], ((ib / kStagesB) & 1) ^ 1);
             mbar_expect_tx(&fullB[sb], kStageB);
@@ -280,7 +301,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     const uint32_t idesc = tc::idesc_f16(std::is_same<T, __nv_bfloat16>::value, BM, BN,
                                          MODE == MODE_DGRAD, false);
     int it = 0, ib = 0, q0 = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, q0 += NSUB) {
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int nsub = item(tile).nsub;
       for (int kb = 0; kb < a.n_kblk; ++kb, ++it) {
         const int s = it % kStagesA;
         mbar_wait(&fullA[s], (it / kStagesA) & 1);
@@ -288,6 +310,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
         const uint32_t a0 = smem_u32(sA + s * kStageA);
 #pragma unroll
         for (int j = 0; j < NSUB; ++j, ++ib) {
+          if (j >= nsub) break;
           const int q = q0 + j, slot = q & 1;
           if (kb == 0) {  // the epilogue has drained this slot's previous sub-tile
             mbar_wait(&tempty_bar[slot], ((q >> 1) & 1) ^ 1);
@@ -313,6 +336,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
         if (lane == 0) tc::commit(&emptyA[s]);
         __syncwarp();
       }
+      q0 += nsub;
     }
   } else if (warp < 2 + kProdWarps) {
     // ================= dequant producers: the A operand =================
@@ -417,11 +441,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       if (++c.kb == per) {
         c.kb = 0;
         c.tile += gridDim.x;
-        c.m_blk += gridDim.x;
-        while (c.m_blk >= a.n_mblk) c.m_blk -= a.n_mblk;
+        if (c.tile < ntiles) c.m_blk = item(c.tile).m_blk;  // once per tile
       }
     };
-    Cursor cl{(int)blockIdx.x, (int)blockIdx.x % a.n_mblk, 0};  // load cursor (2 ahead)
+    Cursor cl{(int)blockIdx.x, item(blockIdx.x).m_blk, 0};  // load cursor (2 ahead)
     Cursor cp = cl;                                              // process cursor
     auto coords = [&](int, int& m_blk, int& kb) {  // next position of the load cursor
       m_blk = cl.m_blk;
@@ -463,8 +486,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     T* stg = sE + ew * 32 * kEpiStride;
     int q = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-    for (int j = 0; j < NSUB; ++j, ++q) {
-      const int m_blk = tile % a.n_mblk, n_blk = tile / a.n_mblk;
+    for (int j = 0; j < item(tile).nsub; ++j, ++q) {
+      const Item ti = item(tile);
+      const int m_blk = ti.m_blk;
       const int acc = q & 1;
       mbar_wait(&tfull_bar[acc], (q >> 1) & 1);
       tc::fence_after();
@@ -478,7 +502,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
         for (int c = 0; c < 32; ++c) stg[c * kEpiStride + lane] = from_f32<T>(__uint_as_float(r[c]));
         __syncwarp();
         // thread = one token, 32 consecutive rows
-        const int tok = n_blk * kTileN + j * BN + cb * 32 + lane;
+        const int tok = ti.tok0 + j * BN + cb * 32 + lane;
         if (tok < a.T) {
           const T* src = stg + lane * kEpiStride;
           if (MODE == MODE_FWD || a.fast_out) {
@@ -725,9 +749,19 @@ int launch_gemm(const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap&
     QEFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  const int tiles = a.n_mblk * a.n_nblk;
-  const int grid = std::min(tiles, num_sms());
-  QEFT_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, m0, m1, mw, a));
+  GemmArgs b = a;
+  const int tiles = a.n_mblk * a.n_nblk, sms = num_sms();
+  b.n_items = b.n_full = tiles;
+  if (NSUB == 2 && tiles > sms) {
+    // split the last partial wave's tiles into halves when they then fit in one wave
+    const int waves = (tiles + sms - 1) / sms, r = tiles - (waves - 1) * sms;
+    if (r < sms && 2 * r <= sms) {
+      b.n_full = (waves - 1) * sms;
+      b.n_items = b.n_full + 2 * r;
+    }
+  }
+  const int grid = std::min(b.n_items, sms);
+  QEFT_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, m0, m1, mw, b));
   return 0;
 }
 

@@ -49,6 +49,9 @@ CASES = [
     (256, 768, 64, 3, 128, "bf16", 700, "structured", False),
     (160, 512, 16, 4, 32, "f16", 520, "irregular", False),
     (128, 384, 32, 4, 64, "bf16", 1000, "structured", True),
+    # 20 m-blocks x 8 token pairs = 160 tiles > 148 SMs: the tail wave runs as half tiles
+    (2560, 512, 64, 4, 128, "bf16", 4000, "structured", False),
+    (512, 2560, 64, 4, 128, "f16", 4000, "structured", False),
 ]
 
 
