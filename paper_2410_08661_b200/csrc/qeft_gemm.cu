@@ -548,32 +548,42 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
 // ---------------------------------------------------------------------------
 // wgrad: dW[o][w] (+)= sum_t dY[t][o] * Xw[t][w]; M = 128 channels, N = k_pad, K = tokens.
 // Both operands MN-major via TMA boxes of {64 (M or N), 64 (t)}.
+// Split-K over tokens runs inside a thread-block cluster: the S CTAs of a cluster (gridDim.x
+// = S, blockIdx.y = channel block) each accumulate their token range in TMEM, stage the fp32
+// partial in their own (now idle) stage memory, and CTA r then sums rows [r*128/S, ...) of
+// all S partials over DSMEM in rank order (deterministic) and writes them to dW. The 128
+// rows of one channel block are one contiguous (128 x k) fp32 chunk of dW, so the
+// read-modify-write is fully coalesced float4 traffic.
+template <int NW>
+struct WgradShape {
+  static constexpr int N = NW * 64;
+  static constexpr int kSA = BM * 64 * 2;  // 16 KB: 2 boxes of 64 channels x 64 tokens
+  static constexpr int kSB = N * 64 * 2;   // NW boxes of 64 weak columns x 64 tokens
+  static constexpr int kStages = (192 * 1024) / (kSA + kSB) > 8 ? 8 : (192 * 1024) / (kSA + kSB);
+  static constexpr int kStride = N + 4;  // staging row pitch (floats): 16-B aligned, conflict-free
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * (kSA + kSB);
+  static_assert((size_t)BM * kStride * 4 <= (size_t)kStages * (kSA + kSB), "staging fits the stages");
+};
+
 template <typename T, int NW>
 __global__ void __launch_bounds__(192, 1)
 wgrad_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_constant__ CUtensorMap map_xw,
-             float* __restrict__ dw, int oc, int k, int T_, int accumulate, int kb_split) {
-  // split-K over tokens: blockIdx.y takes k-blocks [y * kb_split, (y + 1) * kb_split); with
-  // gridDim.y > 1 each split stores its fp32 partial at dw + y * oc * k (a workspace) and
-  // wgrad_reduce_kernel sums the splits in order (deterministic).
-  constexpr int N = NW * 64;
-  constexpr int kSA = BM * 64 * 2;         // 16 KB: 2 boxes of 64 channels x 64 tokens
-  constexpr int kSB = N * 64 * 2;          // NW boxes of 64 weak columns x 64 tokens
-  constexpr int kStages = 4;
+             float* __restrict__ dw, int oc, int k, int T_, int accumulate, int kb_split, int vec_out) {
+  using Sh = WgradShape<NW>;
+  constexpr int N = Sh::N, kSA = Sh::kSA, kSB = Sh::kSB, kStages = Sh::kStages, kStride = Sh::kStride;
   constexpr int kCols = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kSA;
+  float* stg = reinterpret_cast<float*>(smem);  // [128][kStride] fp32 partial, after the mainloop
   __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], done_bar;
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int o0 = blockIdx.x * BM;
-  const int kb0 = blockIdx.y * kb_split;
-  const int nkb = min((T_ + 63) / 64 - kb0, kb_split);
-  if (gridDim.y > 1) {
-    dw += (int64_t)blockIdx.y * oc * k;
-    accumulate = 0;
-  }
+  const int S = gridDim.x, rank = blockIdx.x;  // cluster = the S token splits of one channel block
+  const int o0 = blockIdx.y * BM;
+  const int kb0 = rank * kb_split;
+  const int nkb = max(0, min((T_ + 63) / 64 - kb0, kb_split));
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -615,48 +625,96 @@ wgrad_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_constant__
           tc::mma_f16(tmem, tc::smem_desc_sw128(a0 + 2048 * kk, 8192, 1024),
                       tc::smem_desc_sw128(b0 + 2048 * kk, 8192, 1024), idesc, (kb | kk) ? 1u : 0u);
         tc::commit(&empty_bar[s]);
-        if (kb == nkb - 1) tc::commit(&done_bar);
       }
       __syncwarp();
     }
+    if (lane == 0) {
+      if (nkb > 0) tc::commit(&done_bar);
+      else mbar_arrive(&done_bar);  // empty split: its partial is zero
+    }
+    __syncwarp();
   } else {
+    // TMEM -> staging (thread = channel row, 32 columns per load)
     const int quad = warp & 3;
     mbar_wait(&done_bar, 0);
     tc::fence_after();
-    const int o = o0 + quad * 32 + lane;
+    float* row = stg + (quad * 32 + lane) * kStride;
 #pragma unroll 1
     for (int cb = 0; cb < N / 32; ++cb) {
       uint32_t r[32];
-      tc::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + cb * 32, r);
-      if (o < oc) {
-        float* dst = dw + (int64_t)o * k + cb * 32;
+      if (nkb > 0) {
+        tc::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + cb * 32, r);
+      } else {
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          if (cb * 32 + c < k) {
-            const float v = __uint_as_float(r[c]);
-            dst[c] = accumulate ? dst[c] + v : v;
-          }
-        }
+        for (int c = 0; c < 32; ++c) r[c] = 0u;
       }
+#pragma unroll
+      for (int c = 0; c < 32; c += 4)
+        *reinterpret_cast<float4*>(row + cb * 32 + c) =
+            make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]), __uint_as_float(r[c + 2]),
+                        __uint_as_float(r[c + 3]));
     }
     tc::fence_before();
   }
   __syncthreads();
+  if (S > 1) cluster_sync();  // every split's partial is staged
+  // rows [rank * R, (rank + 1) * R) of the channel block: dW (+)= sum over splits, rank order
+  const int R = BM / S;
+  const uint32_t stg_base = smem_u32(stg);
+  if (vec_out) {
+    // batches of 8 float4 per thread: the dW loads of a batch are in flight together
+    constexpr int C4 = N / 4, kB = 8;
+    const int n4 = R * C4;
+    for (int i0 = 0; i0 < n4; i0 += kB * (int)blockDim.x) {
+      float4 v[kB];
+      float4* dst[kB];
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+        const int i = i0 + b * blockDim.x + threadIdx.x;
+        const int rr = rank * R + i / C4, c = (i % C4) * 4;
+        const bool ok = i < n4 && o0 + rr < oc && c < k;
+        dst[b] = ok ? reinterpret_cast<float4*>(dw + (int64_t)(o0 + rr) * k + c) : nullptr;
+        v[b] = (ok && accumulate) ? *dst[b] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+        if (!dst[b]) continue;
+        const int i = i0 + b * blockDim.x + threadIdx.x;
+        const int rr = rank * R + i / C4, c = (i % C4) * 4;
+        const uint32_t off = stg_base + (uint32_t)(rr * kStride + c) * 4;
+        for (int sp = 0; sp < S; ++sp) {
+          float4 p;
+          if (S == 1) {
+            p = *reinterpret_cast<const float4*>(stg + rr * kStride + c);
+          } else {
+            uint32_t remote;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(off), "r"(sp));
+            asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                         : "=f"(p.x), "=f"(p.y), "=f"(p.z), "=f"(p.w)
+                         : "r"(remote)
+                         : "memory");
+          }
+          v[b].x += p.x; v[b].y += p.y; v[b].z += p.z; v[b].w += p.w;
+        }
+        *dst[b] = v[b];
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < R * N; i += blockDim.x) {
+      const int rr = rank * R + i / N, c = i % N;
+      const int o = o0 + rr;
+      if (o >= oc || c >= k) continue;
+      const uint32_t off = stg_base + (uint32_t)(rr * kStride + c) * 4;
+      float* dst = dw + (int64_t)o * k + c;
+      float v = accumulate ? *dst : 0.f;
+      for (int sp = 0; sp < S; ++sp) v += (S == 1) ? stg[rr * kStride + c] : ld_dsmem_f32(off, sp);
+      *dst = v;
+    }
+  }
+  if (S > 1) cluster_sync();  // keep this CTA's partial alive until every rank has read it
   if (warp == 1) {
     tc::fence_after();
     tc::tmem_dealloc(tmem, kCols);
-  }
-}
-
-// dw[i] (+)= sum_s part[s][i], s = 0..splits-1 in order (deterministic split-K reduction)
-__global__ void wgrad_reduce_kernel(const float* __restrict__ part, float* __restrict__ dw, int64_t n,
-                                    int splits, int accumulate) {
-  pdl_launch_dependents();
-  pdl_wait();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float v = accumulate ? dw[i] : 0.f;
-    for (int s = 0; s < splits; ++s) v += part[(int64_t)s * n + i];
-    dw[i] = v;
   }
 }
 
@@ -811,24 +869,23 @@ GemmArgs base_args(const qeft_linear_t* L, int T_) {
 
 namespace qeft {
 
-// split count for the wgrad token reduction: fill ~2 CTAs per SM, >= 4 k-blocks per split
+// cluster size (token splits) of the wgrad reduction: a power of two <= 8 so that the clusters
+// of all channel blocks fit one wave, with >= 4 k-blocks per split
 int wgrad_splits(int oc, int T_) {
   const int mb = (oc + BM - 1) / BM, nkb = (T_ + 63) / 64;
   static const int forced = getenv("QEFT_WGRAD_SPLITS") ? atoi(getenv("QEFT_WGRAD_SPLITS")) : 0;  // tuning
-  if (forced > 0) return std::max(1, std::min(forced, nkb));
-  // about one CTA per SM: measured on the 7B shapes at T=2048, more splits only add
-  // partial-store traffic (4096 rows: 4 splits 21.9 us vs 8 splits 32.2 us; 11008 rows: 1 split best)
-  int s = num_sms() / mb;
-  s = std::min(s, std::max(1, nkb / 4));
-  return std::max(1, std::min(s, 16));
+  int lim = forced > 0 ? forced : std::min(num_sms() / mb, nkb / 4);
+  lim = std::max(1, std::min(lim, 8));
+  int s = 1;
+  while (s * 2 <= lim) s *= 2;
+  return s;
 }
 
 size_t gemm_workspace_bytes(const qeft_linear_t* L, int T_) {
   // gathered activations in B200 K order (fwd, non-structured layouts), weak columns
   // (wgrad), or a 16-byte-pitched copy of dY (dgrad/wgrad when oc % 8 != 0)
   const size_t kk = (size_t)std::max(L->m_pad + L->k_pad, pad_to(L->oc, 8) + L->k_pad);
-  const size_t part = L->k ? (size_t)wgrad_splits(L->oc, T_) * L->oc * L->k * 4 + 256 : 0;
-  return (size_t)T_ * kk * 2 + part + 1024;
+  return (size_t)T_ * kk * 2 + 1024;
 }
 
 // dY with a row pitch TMA cannot address -> copy into ws with pitch roundup(oc, 8)
@@ -898,9 +955,8 @@ int gemm_dgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, void* dx, i
 
 template <typename T, int NW>
 int launch_wgrad(const CUtensorMap& md, const CUtensorMap& mx, float* dw, int oc, int k, int T_, int acc,
-                 float* part, cudaStream_t st) {
-  constexpr int kStages = 4;
-  const size_t smem = 1024 + (size_t)kStages * (BM * 64 * 2 + NW * 64 * 64 * 2);
+                 cudaStream_t st) {
+  const size_t smem = WgradShape<NW>::kSmem;
   auto kern = wgrad_kernel<T, NW>;
   static bool attr = false;
   if (!attr) {
@@ -908,18 +964,11 @@ int launch_wgrad(const CUtensorMap& md, const CUtensorMap& mx, float* dw, int oc
     attr = true;
   }
   const int nkb = (T_ + 63) / 64;
-  const int splits = part ? wgrad_splits(oc, T_) : 1;
-  const int kbs = (nkb + splits - 1) / splits;
-  const int ns = (nkb + kbs - 1) / kbs;  // splits actually used
-  float* out = ns > 1 ? part : dw;
-  QEFT_CUDA(launch_pdl(kern, dim3((oc + BM - 1) / BM, ns), dim3(192), smem, st, md, mx, out, oc, k, T_, acc,
-                       kbs));
-  if (ns > 1) {
-    const int64_t n = (int64_t)oc * k;
-    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 4 * num_sms());
-    QEFT_CUDA(launch_pdl(wgrad_reduce_kernel, dim3(blocks), dim3(256), 0, st, (const float*)part, dw, n, ns,
-                         acc));
-  }
+  const int S = wgrad_splits(oc, T_);
+  const int kbs = (nkb + S - 1) / S;
+  const int vec = (k % 4 == 0) && (((uintptr_t)dw & 15) == 0);
+  QEFT_CUDA(launch_pdl_cluster(kern, dim3(S, (oc + BM - 1) / BM), dim3(192), smem, st, S, md, mx, dw, oc, k, T_,
+                               acc, kbs, vec));
   return 0;
 }
 
@@ -929,12 +978,9 @@ int gemm_wgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, const void*
   if (L->k == 0) return 0;
   QEFT_CHECK(L->k_pad <= 256, QEFT_ERR_LAYOUT, "gemm_wgrad: k_pad=%d > 256", L->k_pad);
   CUtensorMap md, mx;
-  // workspace: [weak columns of x (T x k_pad)] [split-K partials] [pitched dY copy]
+  // workspace: [weak columns of x (T x k_pad)] [pitched dY copy]
   const size_t xw_bytes = (size_t)T_ * L->k_pad * 2;
-  const size_t part_off = (xw_bytes + 255) & ~(size_t)255;
-  const size_t part_bytes = (size_t)wgrad_splits(L->oc, T_) * L->oc * L->k * 4;
-  float* part = ws_bytes >= part_off + part_bytes ? (float*)((char*)ws + part_off) : nullptr;
-  const size_t dy_off = part ? ((part_off + part_bytes + 255) & ~(size_t)255) : part_off;
+  const size_t dy_off = (xw_bytes + 255) & ~(size_t)255;
   void* ws_dy = (char*)ws + dy_off;
   const size_t ws_dy_bytes = ws_bytes > dy_off ? ws_bytes - dy_off : 0;
   if (int r = pitch_dy(L, dy, lddy, T_, ws_dy, ws_dy_bytes, st)) return r;
@@ -956,8 +1002,8 @@ int gemm_wgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, const void*
   const bool bf = L->act_dtype == QEFT_BF16;
 #define QEFT_WG(NW)                                                                              \
   if (nw == NW)                                                                                  \
-    return bf ? launch_wgrad<__nv_bfloat16, NW>(md, mx, dw, L->oc, L->k, T_, accumulate, part, st) \
-              : launch_wgrad<__half, NW>(md, mx, dw, L->oc, L->k, T_, accumulate, part, st);
+    return bf ? launch_wgrad<__nv_bfloat16, NW>(md, mx, dw, L->oc, L->k, T_, accumulate, st) \
+              : launch_wgrad<__half, NW>(md, mx, dw, L->oc, L->k, T_, accumulate, st);
   QEFT_WG(1) QEFT_WG(2) QEFT_WG(3) QEFT_WG(4)
 #undef QEFT_WG
   set_error("gemm_wgrad: unsupported k_pad");

@@ -52,6 +52,8 @@ CASES = [
     # 20 m-blocks x 8 token pairs = 160 tiles > 148 SMs: the tail wave runs as half tiles
     (2560, 512, 64, 4, 128, "bf16", 4000, "structured", False),
     (512, 2560, 64, 4, 128, "f16", 4000, "structured", False),
+    # k % 4 != 0: scalar wgrad epilogue; 1 channel block -> 8-CTA wgrad cluster
+    (96, 200, 6, 4, 40, "bf16", 600, "structured", False),
 ]
 
 
