@@ -85,6 +85,16 @@ int qeft_gather_cols(const void* x, int64_t ldx, const int32_t* colmap, int kk, 
 int qeft_quantize_rtn(const float* w_dense, int oc, int m, int g, int bits, float* scales,
                       float* zeros, uint8_t* codes, void* stream);
 
+/* alpha-grid search (quantizer.py:144-179, grid_search_group_params): per (row, group) the
+ * range shrink alpha in {alpha_min + i (1 - alpha_min)/(steps - 1)} with least fp64 squared
+ * error (larger alpha on ties), params stored fp32. Bit-exact with the reference (same fp64
+ * op order, numpy pairwise summation of the errors). */
+int qeft_grid_params(const float* w_dense, int oc, int m, int g, int bits, int steps, double alpha_min,
+                     float* scales, float* zeros, void* stream);
+/* nearest codes on fixed fp32 params (quantizer.py:211-218 _nearest_codes), uint8 [oc][m]. */
+int qeft_nearest_codes(const float* w_dense, int oc, int m, int g, int bits, const float* scales,
+                       const float* zeros, uint8_t* codes, void* stream);
+
 /* ---- decode GEMV (kernels.py:87-157 matvec_structured/irregular/online) ----
  * y[n][o] = sum_i W_hat[o][i] * x[n][i] for n < n_cols (1..16), x/y row-major.
  * y is act_dtype, or fp32 when y_f32 != 0. Needs qeft_gemv_workspace_bytes() of

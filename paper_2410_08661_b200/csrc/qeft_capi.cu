@@ -75,6 +75,16 @@ int qeft_gather_cols(const void* x, int64_t ldx, const int32_t* colmap, int kk, 
   return gather_cols(x, ldx, colmap, kk, rows, dt, xb, ST(s));
 }
 
+int qeft_grid_params(const float* w, int oc, int m, int g, int bits, int steps, double alpha_min, float* sc,
+                     float* zr, void* s) {
+  return grid_params(w, oc, m, g, bits, steps, alpha_min, sc, zr, ST(s));
+}
+
+int qeft_nearest_codes(const float* w, int oc, int m, int g, int bits, const float* sc, const float* zr,
+                       uint8_t* codes, void* s) {
+  return nearest_codes(w, oc, m, g, bits, sc, zr, codes, ST(s));
+}
+
 int qeft_quantize_rtn(const float* w, int oc, int m, int g, int bits, float* sc, float* zr,
                       uint8_t* codes, void* s) {
   return quantize_rtn(w, oc, m, g, bits, sc, zr, codes, ST(s));

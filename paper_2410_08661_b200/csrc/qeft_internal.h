@@ -38,6 +38,10 @@ int pack_weak(const float* w, int oc, int k, int dtype, void* out, cudaStream_t 
 int dequant_full(const qeft_linear_t* L, float* out, cudaStream_t st);
 int gather_cols(const void* x, int64_t ldx, const int* colmap, int kk, int rows, int dtype, void* xb,
                 cudaStream_t st);
+int grid_params(const float* w, int oc, int m, int g, int bits, int steps, double amin, float* s, float* z,
+                cudaStream_t st);
+int nearest_codes(const float* w, int oc, int m, int g, int bits, const float* s, const float* z, uint8_t* codes,
+                  cudaStream_t st);
 int quantize_rtn(const float* w, int oc, int m, int g, int bits, float* s, float* z, uint8_t* codes,
                  cudaStream_t st);
 

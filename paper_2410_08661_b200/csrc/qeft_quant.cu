@@ -3,6 +3,8 @@
 // (quantizer.py:211-218): per (row, group) min/max in fp32, scale computed in
 // fp64 and stored fp32, codes = clip(rint((w64 - z) / s), 0, 2^b - 1) in fp64
 // (CUDA rint is round-half-to-even like np.rint).
+#include <algorithm>
+
 #include "qeft_common.cuh"
 #include "qeft_internal.h"
 
@@ -36,9 +38,174 @@ __global__ void rtn_kernel(const float* __restrict__ w, int oc, int m, int g, in
   }
 }
 
+// ---------------------------------------------------------------------------
+// alpha-grid parameter search (quantizer.py:144-179, grid_search_group_params), bit-exact.
+// Every fp64 operation is a separately rounded IEEE op in the reference's order (no FMA
+// contraction), and the squared errors are summed in numpy's pairwise order
+// (np.add.reduce on a contiguous float64 array: 8 running sums over blocks of <= 128
+// elements, halves split at a multiple of 8 above that), so the chosen alpha -- the last
+// minimum, larger alpha on ties -- is the reference's.
+
+struct GridCand {
+  double s, lo;
+};
+
+// error of candidate (s, lo) over w[a, a+n), summed exactly like numpy's pairwise_sum
+QEFT_DEV double grid_err_leaf(const double* w, int a, int n, GridCand c, double levels) {
+  auto e2 = [&](int i) {
+    double q = rint(__ddiv_rn(__dsub_rn(w[i], c.lo), c.s));
+    q = fmin(fmax(q, 0.0), levels);
+    const double d = __dsub_rn(w[i], __dadd_rn(__dmul_rn(q, c.s), c.lo));
+    return __dmul_rn(d, d);
+  };
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, e2(a + i));
+    return r;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = e2(a + j);
+  int i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], e2(a + i + j));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, e2(a + i));
+  return res;
+}
+
+QEFT_DEV double grid_err(const double* w, int a, int n, GridCand c, double levels) {
+  if (n <= 128) return grid_err_leaf(w, a, n, c, levels);
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(grid_err(w, a, n2, c, levels), grid_err(w, a + n2, n - n2, c, levels));
+}
+
+// one warp per (row, group); lanes take alphas i = lane, lane + 32, ...
+__global__ void __launch_bounds__(256) grid_kernel(const float* __restrict__ wq, int oc, int m, int g, int bits,
+                                                   int steps, double amin, float* __restrict__ sc,
+                                                   float* __restrict__ zr) {
+  extern __shared__ double wsh[];  // [8 warps][g]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ng = (m + g - 1) / g;
+  const int64_t item = (int64_t)blockIdx.x * 8 + warp;
+  if (item >= (int64_t)oc * ng) return;
+  const int r = (int)(item / ng), gi = (int)(item % ng);
+  const int a0 = gi * g, n = min(g, m - a0);
+  double* w = wsh + (size_t)warp * g;
+  double mn = INFINITY, mx = -INFINITY;
+  for (int i = lane; i < n; i += 32) {
+    const double v = (double)wq[(int64_t)r * m + a0 + i];
+    w[i] = v;
+    mn = fmin(mn, v);
+    mx = fmax(mx, v);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  __syncwarp();
+  const int64_t out = (int64_t)r * ng + gi;
+  if (mx == mn) {  // constant group: scale 1, zero = wmin (quantizer.py:157-158)
+    if (lane == 0) {
+      sc[out] = 1.f;
+      zr[out] = (float)mn;
+    }
+    return;
+  }
+  const double levels = (double)((1 << bits) - 1);
+  const double mid = __dmul_rn(0.5, __dadd_rn(mn, mx));
+  const double da = __dsub_rn(1.0, amin);
+  double best = INFINITY;
+  int bi = -1;
+  GridCand bc{0.0, 0.0};
+  for (int i = lane; i < steps; i += 32) {
+    // alphas = alpha_min + arange(steps) * (1 - alpha_min) / (steps - 1)   (left to right)
+    const double al = steps == 1 ? 1.0 : __dadd_rn(amin, __ddiv_rn(__dmul_rn((double)i, da), (double)(steps - 1)));
+    double lo, hi;
+    if (al == 1.0) {  // keep the min-max endpoints bit-exact
+      lo = mn;
+      hi = mx;
+    } else {
+      lo = __dsub_rn(mid, __dmul_rn(al, __dsub_rn(mid, mn)));
+      hi = __dadd_rn(mid, __dmul_rn(al, __dsub_rn(mx, mid)));
+    }
+    const GridCand c{__ddiv_rn(__dsub_rn(hi, lo), levels), lo};
+    const double e = grid_err(w, 0, n, c, levels);
+    if (e <= best) {  // increasing i within the lane: later (larger) alpha wins ties
+      best = e;
+      bi = i;
+      bc = c;
+    }
+  }
+  // across lanes: least error, then the larger alpha index
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    const double os = __shfl_xor_sync(0xffffffffu, bc.s, o);
+    const double ol = __shfl_xor_sync(0xffffffffu, bc.lo, o);
+    if (oi >= 0 && (bi < 0 || ob < best || (ob == best && oi > bi))) {
+      best = ob;
+      bi = oi;
+      bc = GridCand{os, ol};
+    }
+  }
+  if (lane == 0) {
+    sc[out] = (float)bc.s;
+    zr[out] = (float)bc.lo;
+  }
+}
+
+// nearest codes on fixed fp32 params (quantizer.py:211-218): clip(rint((w64 - z) / s))
+__global__ void nearest_kernel(const float* __restrict__ w, int oc, int m, int g, int bits,
+                               const float* __restrict__ sc, const float* __restrict__ zr,
+                               uint8_t* __restrict__ codes) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)oc * m) return;
+  const int r = (int)(idx / m), j = (int)(idx % m);
+  const int ng = (m + g - 1) / g;
+  const int gi = min(j / g, ng - 1);
+  const double s = (double)sc[(int64_t)r * ng + gi], z = (double)zr[(int64_t)r * ng + gi];
+  double c = rint(__ddiv_rn(__dsub_rn((double)w[idx], z), s));
+  c = fmin(fmax(c, 0.0), (double)((1 << bits) - 1));
+  codes[idx] = (uint8_t)c;
+}
+
 }  // namespace
 
 namespace qeft {
+
+int grid_params(const float* w, int oc, int m, int g, int bits, int steps, double amin, float* s, float* z,
+                cudaStream_t st) {
+  QEFT_CHECK(bits == 3 || bits == 4, QEFT_ERR_SHAPE, "grid_params: bits=%d", bits);
+  QEFT_CHECK(g >= 1 && steps >= 1, QEFT_ERR_SHAPE, "grid_params: g=%d steps=%d", g, steps);
+  const int ng = m > 0 ? (m + g - 1) / g : 0;
+  const int64_t n = (int64_t)oc * ng;
+  if (!n) return 0;
+  const int gs = std::min(g, m);
+  const size_t smem = (size_t)8 * gs * sizeof(double);
+  QEFT_CHECK(smem <= 200 * 1024, QEFT_ERR_SHAPE, "grid_params: group size %d too large", gs);
+  if (smem > 48 * 1024) QEFT_CUDA(cudaFuncSetAttribute(grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  grid_kernel<<<(unsigned)((n + 7) / 8), 256, smem, st>>>(w, oc, m, gs, bits, steps, amin, s, z);
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int nearest_codes(const float* w, int oc, int m, int g, int bits, const float* s, const float* z, uint8_t* codes,
+                  cudaStream_t st) {
+  QEFT_CHECK(bits == 3 || bits == 4, QEFT_ERR_SHAPE, "nearest_codes: bits=%d", bits);
+  QEFT_CHECK(g >= 1, QEFT_ERR_SHAPE, "nearest_codes: g=%d", g);
+  const int64_t n = (int64_t)oc * m;
+  if (!n) return 0;
+  nearest_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w, oc, m, std::min(g, m), bits, s, z, codes);
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
 
 int quantize_rtn(const float* w, int oc, int m, int g, int bits, float* s, float* z, uint8_t* codes,
                  cudaStream_t st) {

@@ -142,34 +142,19 @@ def _rtn_gpu(w_dense: np.ndarray, g: int, bits: int):
 
 
 def _grid_params_gpu(w_dense: np.ndarray, g: int, bits: int, steps: int, amin: float):
-    """alpha-grid search (quantizer.py:144-179) for every (row, group), fp64 on GPU."""
+    """alpha-grid search (quantizer.py:144-179) for every (row, group): libqeft_b200
+    `qeft_grid_params`, bit-exact with the reference (fp64 op order, numpy pairwise sums)."""
     import torch
     if steps < 1:
         raise ShapeError("grid_steps must be >= 1")
-    w = torch.from_numpy(np.asarray(w_dense, np.float64)).cuda()
-    oc, m = w.shape
-    levels = 2 ** bits - 1
-    alphas = [1.0] if steps == 1 else list(amin + np.arange(steps) * (1.0 - amin) / (steps - 1))
-    al = torch.tensor(alphas, dtype=torch.float64, device="cuda")
-    is_one = al == 1.0
-    sc = torch.empty((oc, _n_groups(m, g)), dtype=torch.float64, device="cuda")
+    oc, m = w_dense.shape
+    ng = _n_groups(m, g)
+    wd = torch.from_numpy(np.ascontiguousarray(w_dense, np.float32)).cuda()
+    sc = torch.empty((oc, ng), dtype=torch.float32, device="cuda")
     zr = torch.empty_like(sc)
-    for gi, (a, b) in enumerate(group_slices(m, g)):
-        seg = w[:, a:b]
-        wmin, wmax = seg.min(dim=1).values[:, None], seg.max(dim=1).values[:, None]
-        mid = 0.5 * (wmin + wmax)
-        lo = torch.where(is_one[None], wmin, mid - al[None] * (mid - wmin))
-        hi = torch.where(is_one[None], wmax, mid + al[None] * (wmax - mid))
-        s = (hi - lo) / levels                                      # (oc, A)
-        c = torch.clamp(torch.round((seg[:, None, :] - lo[..., None]) / s[..., None]), 0, levels)
-        err = ((seg[:, None, :] - (c * s[..., None] + lo[..., None])) ** 2).sum(-1)
-        pick = (err.shape[1] - 1) - torch.argmin(err.flip(1), dim=1)  # last min: larger alpha wins ties
-        s_best = s.gather(1, pick[:, None])[:, 0]
-        z_best = lo.gather(1, pick[:, None])[:, 0]
-        const = (wmax == wmin)[:, 0]
-        sc[:, gi] = torch.where(const, torch.ones_like(s_best), s_best)
-        zr[:, gi] = torch.where(const, wmin[:, 0], z_best)
-    return sc.float().cpu().numpy(), zr.float().cpu().numpy()
+    _lib.check(_lib.lib().qeft_grid_params(_lib.ptr(wd), oc, m, g, bits, int(steps), float(amin),
+                                           _lib.ptr(sc), _lib.ptr(zr), _lib.stream_ptr()), "grid_params")
+    return sc.cpu().numpy(), zr.cpu().numpy()
 
 
 def _optq_gpu(w_dense, h, sc, zr, g, bits):
@@ -202,15 +187,16 @@ def _optq_gpu(w_dense, h, sc, zr, g, bits):
 
 
 def _nearest_codes_gpu(w_dense, sc, zr, g, bits):
-    """Independent nearest rounding on fixed params (quantizer.py:211-218), fp64 on GPU."""
+    """Independent nearest rounding on fixed params (quantizer.py:211-218): `qeft_nearest_codes`."""
     import torch
     oc, m = w_dense.shape
-    gidx = torch.clamp(torch.arange(m, device="cuda") // g, max=max(_n_groups(m, g) - 1, 0))
-    w = torch.from_numpy(np.asarray(w_dense, np.float64)).cuda()
-    s = torch.from_numpy(sc.astype(np.float64)).cuda()[:, gidx]
-    z = torch.from_numpy(zr.astype(np.float64)).cuda()[:, gidx]
-    c = torch.clamp(torch.round((w - z) / s), 0, 2 ** bits - 1)
-    return c.to(torch.uint8).cpu().numpy()
+    wd = torch.from_numpy(np.ascontiguousarray(w_dense, np.float32)).cuda()
+    s = torch.from_numpy(np.ascontiguousarray(sc, np.float32)).cuda()
+    z = torch.from_numpy(np.ascontiguousarray(zr, np.float32)).cuda()
+    codes = torch.empty((oc, m), dtype=torch.uint8, device="cuda")
+    _lib.check(_lib.lib().qeft_nearest_codes(_lib.ptr(wd), oc, m, g, bits, _lib.ptr(s), _lib.ptr(z),
+                                             _lib.ptr(codes), _lib.stream_ptr()), "nearest_codes")
+    return codes.cpu().numpy()
 
 
 def quantize_layer(w, *, k: int, bits: int, g: int, mode: str = "optq",

@@ -122,6 +122,18 @@ def gen_quantizer():
     d["grid_segs"] = segs
     d["grid_scale"] = np.array([p.scale for p in gp])
     d["grid_zero"] = np.array([p.zero for p in gp])
+    # fp32-valued segments (what quantize_layer feeds the search), incl. ragged/odd lengths
+    segs32 = (rng.standard_normal((40, 128)) * 0.05).astype(np.float32)
+    segs32[3, :] = segs32[3, 0]                  # constant group
+    segs32[5, 7] = 3.0                           # outlier
+    gp32 = [quantizer.grid_search_group_params(s.astype(np.float64), 4) for s in segs32]
+    gp32_3 = [quantizer.grid_search_group_params(s[:53].astype(np.float64), 3) for s in segs32]
+    d["grid_segs32"] = segs32
+    d["grid_scale32"] = np.array([np.float32(p.scale) for p in gp32])
+    d["grid_zero32"] = np.array([np.float32(p.zero) for p in gp32])
+    d["grid_scale32_b3_n53"] = \
+        np.array([np.float32(p.scale) for p in gp32_3])
+    d["grid_zero32_b3_n53"] = np.array([np.float32(p.zero) for p in gp32_3])
     d["n"] = n
     np.savez_compressed(os.path.join(OUT, "quantizer.npz"), **d)
 

@@ -74,6 +74,12 @@ def test_grid_search_golden():
     for i, seg in enumerate(z["grid_segs"]):
         s, zz = O.grid_scale_zero(seg, 4)
         assert s == z["grid_scale"][i] and zz == z["grid_zero"][i]
+    # fp32-valued segments (the quantize_layer input type), 4-bit and 3-bit over 53 values
+    for i, seg in enumerate(z["grid_segs32"]):
+        s, zz = O.grid_scale_zero(seg, 4)
+        assert np.float32(s) == z["grid_scale32"][i] and np.float32(zz) == z["grid_zero32"][i]
+        s, zz = O.grid_scale_zero(seg[:53], 3)
+        assert np.float32(s) == z["grid_scale32_b3_n53"][i] and np.float32(zz) == z["grid_zero32_b3_n53"][i]
     # grid_steps=1 is min-max (pkg/tests/test_quantizer.py:59-63)
     seg = z["grid_segs"][0]
     assert O.grid_scale_zero(seg, 4, steps=1) == O.minmax_scale_zero(seg, 4)
