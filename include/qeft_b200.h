@@ -95,6 +95,13 @@ int qeft_grid_params(const float* w_dense, int oc, int m, int g, int bits, int s
 int qeft_nearest_codes(const float* w_dense, int oc, int m, int g, int bits, const float* scales,
                        const float* zeros, uint8_t* codes, void* stream);
 
+/* OPTQ greedy rounding (quantizer.py:221-259 optq_quantize) given the reference's factor
+ * u64 = chol(inv(H_damped)).T [m][m] (host numpy, as the reference computes it). w64 [oc][m]
+ * is the fp64 working copy (overwritten); err_ws is oc*m fp64 scratch. Codes uint8 [oc][m],
+ * bit-exact: each weight gets its updates in the reference's order with separate roundings. */
+int qeft_optq_codes(double* w64, const double* u64, const float* scales, const float* zeros, int oc, int m,
+                    int g, int bits, double* err_ws, uint8_t* codes, void* stream);
+
 /* ---- decode GEMV (kernels.py:87-157 matvec_structured/irregular/online) ----
  * y[n][o] = sum_i W_hat[o][i] * x[n][i] for n < n_cols (1..16), x/y row-major.
  * y is act_dtype, or fp32 when y_f32 != 0. Needs qeft_gemv_workspace_bytes() of

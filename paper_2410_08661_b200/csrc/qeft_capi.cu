@@ -85,6 +85,11 @@ int qeft_nearest_codes(const float* w, int oc, int m, int g, int bits, const flo
   return nearest_codes(w, oc, m, g, bits, sc, zr, codes, ST(s));
 }
 
+int qeft_optq_codes(double* w64, const double* u64, const float* sc, const float* zr, int oc, int m, int g,
+                    int bits, double* err_ws, uint8_t* codes, void* s) {
+  return optq_codes(w64, u64, sc, zr, oc, m, g, bits, err_ws, codes, ST(s));
+}
+
 int qeft_quantize_rtn(const float* w, int oc, int m, int g, int bits, float* sc, float* zr,
                       uint8_t* codes, void* s) {
   return quantize_rtn(w, oc, m, g, bits, sc, zr, codes, ST(s));

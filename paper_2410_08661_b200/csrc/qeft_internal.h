@@ -42,6 +42,8 @@ int grid_params(const float* w, int oc, int m, int g, int bits, int steps, doubl
                 cudaStream_t st);
 int nearest_codes(const float* w, int oc, int m, int g, int bits, const float* s, const float* z, uint8_t* codes,
                   cudaStream_t st);
+int optq_codes(double* w, const double* u, const float* s, const float* z, int oc, int m, int g, int bits,
+               double* err, uint8_t* codes, cudaStream_t st);
 int quantize_rtn(const float* w, int oc, int m, int g, int bits, float* s, float* z, uint8_t* codes,
                  cudaStream_t st);
 

@@ -176,9 +176,107 @@ __global__ void nearest_kernel(const float* __restrict__ w, int oc, int m, int g
   codes[idx] = (uint8_t)c;
 }
 
+// ---------------------------------------------------------------------------
+// OPTQ greedy rounding (quantizer.py:221-259, optq_quantize), bit-exact given the reference's
+// U = chol(inv(H_damped)).T (computed on the host by numpy, as the reference does). Every
+// weight w[r][j] receives the updates w -= err[r][i] * U[i][j] for i = 0 .. j-1 in increasing
+// i, each as a rounded multiply then a rounded subtract -- the reference's
+// `w[:, i+1:] -= np.outer(err, u[i, i+1:])` sequence. Left-looking blocks of kOptqB columns:
+//   optq_update_kernel: apply to block [j0, j0+B) the errors of all columns < j0 (in order),
+//   optq_block_kernel:  one thread per row walks the block sequentially (codes, err, in-block
+//                       updates).
+constexpr int kOptqB = 64;
+
+__global__ void __launch_bounds__(256) optq_update_kernel(double* __restrict__ W, const double* __restrict__ E,
+                                                          const double* __restrict__ U, int oc, int m, int j0,
+                                                          int j1) {
+  // tile: 32 columns x 64 rows; thread -> column c, rows r0 + 8 * (t / 32) + 0..7
+  __shared__ double Es[64][33];
+  __shared__ double Us[32][33];
+  const int t = threadIdx.x, c = t & 31, rq = t >> 5;
+  const int col = j0 + blockIdx.x * 32 + c;
+  const int r0 = blockIdx.y * 64;
+  double w[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int r = r0 + rq * 8 + q;
+    w[q] = (r < oc && col < j1) ? W[(int64_t)r * m + col] : 0.0;
+  }
+  for (int i0 = 0; i0 < j0; i0 += 32) {
+    const int ni = min(32, j0 - i0);
+    for (int e = t; e < 64 * 32; e += 256) {  // E[r0 .. r0+63][i0 .. i0+31]
+      const int rr = e >> 5, ii = e & 31, r = r0 + rr;
+      Es[rr][ii] = (r < oc && ii < ni) ? E[(int64_t)r * m + i0 + ii] : 0.0;
+    }
+    for (int e = t; e < 32 * 32; e += 256) {  // U[i0 .. i0+31][block columns]
+      const int ii = e >> 5, cc = e & 31, cj = j0 + blockIdx.x * 32 + cc;
+      Us[ii][cc] = (ii < ni && cj < j1) ? U[(int64_t)(i0 + ii) * m + cj] : 0.0;
+    }
+    __syncthreads();
+    for (int ii = 0; ii < ni; ++ii) {
+      const double u = Us[ii][c];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) w[q] = __dsub_rn(w[q], __dmul_rn(Es[rq * 8 + q][ii], u));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int r = r0 + rq * 8 + q;
+    if (r < oc && col < j1) W[(int64_t)r * m + col] = w[q];
+  }
+}
+
+__global__ void __launch_bounds__(128) optq_block_kernel(const double* __restrict__ W, double* __restrict__ E,
+                                                         const double* __restrict__ U, const float* __restrict__ sc,
+                                                         const float* __restrict__ zr, uint8_t* __restrict__ codes,
+                                                         int oc, int m, int g, int ng, int bits, int j0) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= oc) return;
+  const int nb = min(kOptqB, m - j0);
+  const double levels = (double)((1 << bits) - 1);
+  double w[kOptqB];
+#pragma unroll
+  for (int k = 0; k < kOptqB; ++k) w[k] = k < nb ? W[(int64_t)r * m + j0 + k] : 0.0;
+#pragma unroll
+  for (int i = 0; i < kOptqB; ++i) {
+    if (i >= nb) break;
+    const int col = j0 + i;
+    const int gi = min(col / g, ng - 1);
+    const double s = (double)sc[(int64_t)r * ng + gi], z = (double)zr[(int64_t)r * ng + gi];
+    double c = rint(__ddiv_rn(__dsub_rn(w[i], z), s));
+    c = fmin(fmax(c, 0.0), levels);
+    codes[(int64_t)r * m + col] = (uint8_t)c;
+    const double dq = __dadd_rn(__dmul_rn(c, s), z);
+    const double err = __ddiv_rn(__dsub_rn(w[i], dq), U[(int64_t)col * m + col]);
+    E[(int64_t)r * m + col] = err;
+#pragma unroll
+    for (int j = i + 1; j < kOptqB; ++j)
+      if (j < nb) w[j] = __dsub_rn(w[j], __dmul_rn(err, U[(int64_t)col * m + j0 + j]));
+  }
+}
+
 }  // namespace
 
 namespace qeft {
+
+int optq_codes(double* w, const double* u, const float* s, const float* z, int oc, int m, int g, int bits,
+               double* err, uint8_t* codes, cudaStream_t st) {
+  QEFT_CHECK(bits == 3 || bits == 4, QEFT_ERR_SHAPE, "optq_codes: bits=%d", bits);
+  QEFT_CHECK(g >= 1, QEFT_ERR_SHAPE, "optq_codes: g=%d", g);
+  if (!oc || !m) return 0;
+  const int ge = std::min(g, m), ng = (m + ge - 1) / ge;
+  for (int j0 = 0; j0 < m; j0 += kOptqB) {
+    const int j1 = std::min(m, j0 + kOptqB);
+    if (j0 > 0) {
+      optq_update_kernel<<<dim3((j1 - j0 + 31) / 32, (oc + 63) / 64), 256, 0, st>>>(w, err, u, oc, m, j0, j1);
+      QEFT_CUDA(cudaGetLastError());
+    }
+    optq_block_kernel<<<(oc + 127) / 128, 128, 0, st>>>(w, err, u, s, z, codes, oc, m, ge, ng, bits, j0);
+    QEFT_CUDA(cudaGetLastError());
+  }
+  return 0;
+}
 
 int grid_params(const float* w, int oc, int m, int g, int bits, int steps, double amin, float* s, float* z,
                 cudaStream_t st) {

@@ -157,32 +157,36 @@ def _grid_params_gpu(w_dense: np.ndarray, g: int, bits: int, steps: int, amin: f
     return sc.cpu().numpy(), zr.cpu().numpy()
 
 
-def _optq_gpu(w_dense, h, sc, zr, g, bits):
-    """Greedy OPTQ rounding (quantizer.py:221-259) in fp64 on the GPU."""
-    import torch
-    w = torch.from_numpy(np.array(w_dense, np.float64)).cuda()
-    oc, m = w.shape
-    hd = torch.from_numpy(np.array(h, np.float64)).cuda()
-    hd.diagonal().add_(OPTQ_DAMP_FRAC * float(hd.diagonal().mean()))
+def _optq_factor(h):
+    """U = chol(inv(H + 1% mean-diag damping)).T exactly as the reference computes it on the host
+    (quantizer.py:236-242); None where the reference falls back (LinAlgError)."""
+    hd = np.asarray(h, dtype=np.float64).copy()
+    m = hd.shape[0]
+    damp = OPTQ_DAMP_FRAC * float(np.mean(np.diagonal(hd)))
+    hd[np.diag_indices(m)] += damp
     try:
-        u = torch.linalg.cholesky(torch.linalg.inv(hd)).T.contiguous()
-        if not torch.isfinite(u).all():
-            raise RuntimeError("non-finite factor")
-    except RuntimeError:
+        hinv = np.linalg.inv(hd)
+        return np.ascontiguousarray(np.linalg.cholesky(hinv).T)
+    except np.linalg.LinAlgError:
         return None
-    s64 = torch.from_numpy(sc.astype(np.float64)).cuda()
-    z64 = torch.from_numpy(zr.astype(np.float64)).cuda()
-    ng = s64.shape[1]
+
+
+def _optq_gpu(w_dense, h, sc, zr, g, bits):
+    """Greedy OPTQ rounding (quantizer.py:221-259): the O(oc*m^2) column sweep runs in
+    libqeft_b200 (`qeft_optq_codes`), bit-exact given the host factor."""
+    import torch
+    u = _optq_factor(h)
+    if u is None:
+        return None
+    oc, m = w_dense.shape
+    w = torch.from_numpy(np.array(w_dense, np.float64)).cuda()
+    ud = torch.from_numpy(u).cuda()
+    s = torch.from_numpy(np.ascontiguousarray(sc, np.float32)).cuda()
+    z = torch.from_numpy(np.ascontiguousarray(zr, np.float32)).cuda()
+    err = torch.empty((oc, m), dtype=torch.float64, device="cuda")
     codes = torch.empty((oc, m), dtype=torch.uint8, device="cuda")
-    levels = 2 ** bits - 1
-    for i in range(m):
-        gi = min(i // g, ng - 1)
-        col = w[:, i]
-        q = torch.clamp(torch.round((col - z64[:, gi]) / s64[:, gi]), 0, levels)
-        codes[:, i] = q.to(torch.uint8)
-        e = (col - (q * s64[:, gi] + z64[:, gi])) / u[i, i]
-        if i + 1 < m:
-            w[:, i + 1:].sub_(torch.outer(e, u[i, i + 1:]))
+    _lib.check(_lib.lib().qeft_optq_codes(_lib.ptr(w), _lib.ptr(ud), _lib.ptr(s), _lib.ptr(z), oc, m, g, bits,
+                                          _lib.ptr(err), _lib.ptr(codes), _lib.stream_ptr()), "optq_codes")
     return codes.cpu().numpy()
 
 

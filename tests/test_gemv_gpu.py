@@ -104,7 +104,9 @@ def test_quantize_optq_matches_reference(B):
         c1, c2 = q.codes(), ref.codes()
         total += c1.size
         same += int(np.sum(c1 == c2))
-    assert same / total >= 0.99
+    # the sweep is bit-exact given the factor; the factor comes from this host's LAPACK, which
+    # can differ in the last bits from the machine that wrote the fixture
+    assert same / total >= 0.999
 
 
 # ---------------------------------------------------------------- GEMV -------

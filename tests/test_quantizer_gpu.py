@@ -68,3 +68,33 @@ def test_grid_cfg1_layer_bit_exact(Q):
     sc, zr = Q._grid_params_gpu(w, 128, 4, 100, 0.5)
     so, zo = _oracle_params(w, 128, 4, 100, 0.5)
     assert np.array_equal(sc, so) and np.array_equal(zr, zo)
+
+
+@pytest.mark.parametrize("oc,m,g,bits", [
+    (96, 320, 64, 4),     # 5 blocks of 64 columns
+    (130, 200, 48, 3),    # ragged groups and a partial last block, rows not a multiple of 64
+    (64, 1000, 128, 4),   # 16 blocks, ragged last group
+])
+def test_optq_codes_bit_exact(Q, oc, m, g, bits):
+    """OPTQ codes equal the reference loop's (oracle port, same machine -> same LAPACK factor)."""
+    rng = np.random.default_rng(oc + m)
+    w = (rng.standard_normal((oc, m)) * 0.05).astype(np.float32)
+    x = rng.standard_normal((m, 4 * m // 3))
+    x[rng.choice(m, m // 16, replace=False)] *= 10.0
+    h = 2.0 * x @ x.T
+    sc, zr = Q._grid_params_gpu(w, g, bits, 100, 0.5)
+    codes = Q._optq_gpu(w, h, sc, zr, g, bits)
+    ref, fb = O.optq_codes(w, h, sc, zr, g, bits)
+    assert not fb
+    assert np.array_equal(codes, ref), (np.mean(codes == ref), np.argwhere(codes != ref)[:5])
+
+
+def test_optq_fallback_on_singular_hessian(Q):
+    """A non-positive-definite damped Hessian falls back to nearest rounding (quantizer.py:242-243)."""
+    m = 64
+    w = (np.random.default_rng(3).standard_normal((32, m)) * 0.05).astype(np.float32)
+    h = -np.eye(m)
+    sc, zr = Q._grid_params_gpu(w, 32, 4, 100, 0.5)
+    assert Q._optq_gpu(w, h, sc, zr, 32, 4) is None
+    q = Q.quantize_layer(np.concatenate([w, w[:, :8]], 1), k=8, bits=4, g=32, mode="optq", h=-np.eye(72))
+    assert q.optq_fallback
