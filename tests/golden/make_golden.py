@@ -275,10 +275,34 @@ def gen_finetune():
     np.savez_compressed(os.path.join(OUT, "finetune.npz"), **d)
 
 
+def gen_container():
+    """.qeft files written by the reference's save_checkpoint (container.py:311-319) for the
+    toy quantized models of gen_finetune (OGR with plan + GWC + irregular wo; online with
+    input permutations), plus the reference engine's logits on a fixed batch."""
+    from qeft import container as C
+    from qeft import model as M
+    from qeft import qmodel as Q
+    cfg = M.ModelConfig(d_model=32, n_heads=4, head_dim=8, d_ff=64, n_blocks=2,
+                        vocab_size=256, max_seq=64, seed=5)
+    dense = M.init_model(cfg)
+    ids = np.random.default_rng(77).integers(0, 256, size=4000).astype(np.int64)
+    hess = calibration.collect_calibration(dense, ids, n_seq=4, seq_len=48, seed=0)
+    d = {}
+    for reo in ("ogr", "online"):
+        qm = Q.quantize_model(dense, hess, k=4, bits=4, g=16, mode="rtn", reorder=reo)
+        path = os.path.join(OUT, f"toy_{reo}.qeft")
+        C.save_checkpoint(path, qm)
+        xb, _ = M.sample_windows(np.random.default_rng(13), ids, 2, 24)
+        em = Q.quant_engine(qm, op_factory=lambda nm, q: tuning.QuantLinearTrainOp(nm, q))
+        logits, _, _ = M.forward_batch(em, xb, want_cache=False)
+        d[f"{reo}_xb"], d[f"{reo}_logits"] = xb, logits
+    np.savez_compressed(os.path.join(OUT, "container.npz"), **d)
+
+
 if __name__ == "__main__":
     # `make_golden.py [packing quantizer training selection finetune]` (default: all)
     gens = {"packing": gen_packing, "quantizer": gen_quantizer, "training": gen_training,
-            "selection": gen_selection, "finetune": gen_finetune}
+            "selection": gen_selection, "finetune": gen_finetune, "container": gen_container}
     for name in (sys.argv[1:] or list(gens)):
         gens[name]()
     for f in sorted(os.listdir(OUT)):
