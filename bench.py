@@ -296,6 +296,8 @@ def run_b200(args):
     n_layers = len(layers)
     del stack, layers
     torch.cuda.empty_cache()
+    ds = None if (args.no_dstep or rank != 0) else decode_step_bench(args, torch)
+    torch.cuda.empty_cache()
     ft = None if args.no_ft else finetune_bench(args, ws, rank, dev, torch)
     line = None
     if rank == 0:
@@ -332,6 +334,7 @@ def run_b200(args):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "finetune": ft,
+            "decode_step": ds,
         }
         line["e2e"]["h2d_bytes_per_step"] = sum(2 * n * ic for ic in sorted({s[1] for s in BLOCK_SHAPES}))
         line["e2e"]["d2h_bytes_per_step"] = sum(2 * n * oc for oc, _ in BLOCK_SHAPES) * args.blocks
@@ -339,6 +342,40 @@ def run_b200(args):
     if ws > 1:
         torch.distributed.destroy_process_group()
     return line
+
+
+def decode_step_bench(args, torch):
+    """Whole decode step around the GEMV: 7B-shaped QEFTDecoder, batch 1,
+    KV cache at `--dstep-ctx` tokens. One CUDA graph per step covers norms, q/k/v and
+    gate/up as fused GEMV launches, rotary, the cache write, attention, o/down, SiLU*mul, the
+    dense head and residuals. Device-timed with CUDA events; the GEMV stack's share is the
+    headline value's step time over this one."""
+    from paper_2410_08661_b200.generate import KVDecoder
+    from paper_2410_08661_b200.model import QEFTDecoder
+    from paper_2410_08661_b200.qmodel import LLAMA2_7B
+    model = QEFTDecoder.synthetic(LLAMA2_7B, k=128, bits=4, g=128, act_dtype="f16", compute_dtype="f16")
+    for p in model.parameters():
+        p.requires_grad_(False)
+    ctx, steps = args.dstep_ctx, 32
+    dec = KVDecoder(model, max_seq=ctx + steps + 1, capture=True)
+    tok = torch.tensor([1])
+    for p in range(ctx):  # fill the cache (untimed)
+        dec.step(tok, p)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for i in range(steps):
+        dec.step(tok, ctx + i)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    del dec, model
+    return {"metric": "QEFT greedy decode tokens/s (batch 1)", "value": 1e3 / ms, "unit": "tokens/s",
+            "ms_per_token": ms, "steps": steps,
+            "config": {"workload": "LLaMA-2-7B-shaped QEFT decoder (4-bit g128 k=128, 32 blocks, fp16), "
+                                   "KV cache, one CUDA graph per step",
+                       "context": ctx, "batch": 1},
+            "data": "synthetic", "dtype": "f16"}
 
 
 def finetune_bench(args, ws, rank, local, torch):
@@ -483,6 +520,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ft", action="store_true", help="skip the fine-tune step measurement")
     ap.add_argument("--no-fuse", action="store_true", help="one GEMV launch per layer (no q/k/v, gate/up grouping)")
+    ap.add_argument("--no-dstep", action="store_true", help="skip the end-to-end decode step measurement")
+    ap.add_argument("--dstep-ctx", type=int, default=512)
     ap.add_argument("--ft-blocks", type=int, default=32)
     ap.add_argument("--ft-seq", type=int, default=2048)
     ap.add_argument("--ft-mb", type=int, default=1)

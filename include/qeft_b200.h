@@ -168,7 +168,7 @@ int qeft_weak_shadow(const float* w32, const qeft_shadow_desc_t* descs, int n_la
  * rmsnorm_bwd: dx = gain*dy*rstd - x*rstd^3*sum(gain*dy*x)/C (+ dres if non-NULL).
  * rope: rotate (j, j + hd/2) pairs of every head of rows = B*T tokens (token t = row % T) by
  *       angle t*inv_freq[j] using cos/sin tables [T][hd/2]; inverse != 0 rotates back (backward);
- *       hd % 16 == 0.
+ *       hd even (16-byte vector path when hd % 16 == 0).
  * silu_mul: f = silu(g) * u and (dg, du) from df; n % 8 == 0. */
 int qeft_rmsnorm_fwd(const void* x, const float* gain, void* y, float* rstd, int rows, int C, int dt, void* stream);
 int qeft_rmsnorm_bwd(const void* dy, const void* x, const float* gain, const float* rstd, const void* dres,

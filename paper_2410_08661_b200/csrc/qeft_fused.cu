@@ -4,6 +4,8 @@
 // with fp32 math. Gains are frozen in weak-column tuning (tuning.py:187-248,
 // backward_batch with param_grads=False), so the RMS-norm backward returns dX only.
 // HBM-bound: each kernel reads and writes every element once.
+#include <type_traits>
+
 #include "qeft_common.cuh"
 #include "qeft_internal.h"
 
@@ -114,7 +116,8 @@ __global__ void rmsnorm_bwd_kernel(const T* __restrict__ dy, const T* __restrict
 // angle t * inv_freq[j] (model.py:256-259); dir = -1 applies the inverse (backward).
 // One CTA per token row: the row's cos/sin are read once, 8 pairs per thread-iteration with
 // 16-byte accesses (hd/2 % 8 == 0).
-template <typename T>
+// P pairs per thread: 8 (16-byte vectors, head_dim % 16 == 0) or 1 (any even head_dim)
+template <typename T, int P>
 __global__ void rope_kernel(const T* __restrict__ in, T* __restrict__ out, const float* __restrict__ cosv,
                             const float* __restrict__ sinv, int T_, int H, int hd, float dir) {
   const int half = hd >> 1;
@@ -122,26 +125,32 @@ __global__ void rope_kernel(const T* __restrict__ in, T* __restrict__ out, const
   const int t = (int)(row % T_);
   const float* cr = cosv + (int64_t)t * half;
   const float* sr = sinv + (int64_t)t * half;
-  const int chunks = half >> 3;  // 8-pair chunks per head
+  const int chunks = half / P;  // P-pair chunks per head
   for (int e = threadIdx.x; e < H * chunks; e += blockDim.x) {
-    const int h = e / chunks, j = (e - h * chunks) * 8;
+    const int h = e / chunks, j = (e - h * chunks) * P;
     const int64_t base = (row * H + h) * hd;
-    const uint4 av = *reinterpret_cast<const uint4*>(in + base + j);
-    const uint4 bv = *reinterpret_cast<const uint4*>(in + base + j + half);
-    const T* ae = reinterpret_cast<const T*>(&av);
-    const T* be = reinterpret_cast<const T*>(&bv);
-    uint4 oa, ob;
-    T* oae = reinterpret_cast<T*>(&oa);
-    T* obe = reinterpret_cast<T*>(&ob);
+    T ae[P], be[P], oae[P], obe[P];
+    if constexpr (P == 8) {
+      *reinterpret_cast<uint4*>(ae) = *reinterpret_cast<const uint4*>(in + base + j);
+      *reinterpret_cast<uint4*>(be) = *reinterpret_cast<const uint4*>(in + base + j + half);
+    } else {
+      ae[0] = in[base + j];
+      be[0] = in[base + j + half];
+    }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < P; ++i) {
       const float c = cr[j + i], s = dir * sr[j + i];
       const float a = to_f32<T>(ae[i]), b = to_f32<T>(be[i]);
       oae[i] = from_f32<T>(a * c - b * s);
       obe[i] = from_f32<T>(a * s + b * c);
     }
-    *reinterpret_cast<uint4*>(out + base + j) = oa;
-    *reinterpret_cast<uint4*>(out + base + j + half) = ob;
+    if constexpr (P == 8) {
+      *reinterpret_cast<uint4*>(out + base + j) = *reinterpret_cast<const uint4*>(oae);
+      *reinterpret_cast<uint4*>(out + base + j + half) = *reinterpret_cast<const uint4*>(obe);
+    } else {
+      out[base + j] = oae[0];
+      out[base + j + half] = obe[0];
+    }
   }
 }
 
@@ -227,15 +236,23 @@ int rmsnorm_bwd(const void* dy, const void* x, const float* gain, const float* r
 
 int rope(const void* in, void* out, const float* cosv, const float* sinv, int64_t rows, int T_, int H, int hd,
          int inverse, int dt, cudaStream_t st) {
-  QEFT_CHECK(hd % 16 == 0 && T_ > 0, QEFT_ERR_SHAPE, "rope: head_dim %d must be a multiple of 16", hd);
+  QEFT_CHECK(hd % 2 == 0 && hd > 0 && T_ > 0, QEFT_ERR_SHAPE, "rope: head_dim %d must be even", hd);
   if (!rows) return 0;
   const float dir = inverse ? -1.f : 1.f;
-  const int thr = std::min(256, std::max(32, H * (hd / 16)));
-  if (dt == QEFT_BF16)
-    rope_kernel<__nv_bfloat16><<<(unsigned)rows, thr, 0, st>>>((const __nv_bfloat16*)in, (__nv_bfloat16*)out, cosv,
-                                                               sinv, T_, H, hd, dir);
-  else
-    rope_kernel<__half><<<(unsigned)rows, thr, 0, st>>>((const __half*)in, (__half*)out, cosv, sinv, T_, H, hd, dir);
+  const bool vec = hd % 16 == 0 && ((uintptr_t)in & 15) == 0 && ((uintptr_t)out & 15) == 0;
+  const int thr = std::min(256, std::max(32, H * (vec ? hd / 16 : hd / 2)));
+  auto go = [&](auto tag, auto p) {
+    using T = decltype(tag);
+    rope_kernel<T, decltype(p)::value><<<(unsigned)rows, thr, 0, st>>>((const T*)in, (T*)out, cosv, sinv, T_, H, hd,
+                                                                       dir);
+  };
+  if (dt == QEFT_BF16) {
+    if (vec) go(__nv_bfloat16{}, std::integral_constant<int, 8>{});
+    else go(__nv_bfloat16{}, std::integral_constant<int, 1>{});
+  } else {
+    if (vec) go(__half{}, std::integral_constant<int, 8>{});
+    else go(__half{}, std::integral_constant<int, 1>{});
+  }
   QEFT_CUDA(cudaGetLastError());
   return 0;
 }

@@ -296,6 +296,13 @@ def gen_container():
         em = Q.quant_engine(qm, op_factory=lambda nm, q: tuning.QuantLinearTrainOp(nm, q))
         logits, _, _ = M.forward_batch(em, xb, want_cache=False)
         d[f"{reo}_xb"], d[f"{reo}_logits"] = xb, logits
+        # greedy generation through the reference harness (kernels.py:197-228) and the logits
+        # of every position of the final sequence (what each decode step must reproduce)
+        prompt = ids[100:106]
+        gen = kernels.bench_generate(qm, prompt, 10)
+        seq = np.concatenate([prompt, gen.tokens])[None, :-1]
+        glog, _, _ = M.forward_batch(em, seq, want_cache=False)
+        d[f"{reo}_prompt"], d[f"{reo}_gen_tokens"], d[f"{reo}_gen_logits"] = prompt, gen.tokens, glog
     np.savez_compressed(os.path.join(OUT, "container.npz"), **d)
 
 

@@ -41,11 +41,12 @@ def test_rmsnorm_fwd_bwd(torch_, dt):
     assert rel_err(_np(x.grad), _np(xr.grad)) <= 1e-2
 
 
-def test_rope_fwd_bwd(torch_):
+@pytest.mark.parametrize("hd", [128, 8, 6])  # 16-byte vector path, then the per-pair path
+def test_rope_fwd_bwd(torch_, hd):
     torch = torch_
     from paper_2410_08661_b200 import fused
     from paper_2410_08661_b200.model import rope_tables
-    B, T, H, hd = 2, 65, 4, 128
+    B, T, H = 2, 65, 4
     cos, sin = rope_tables(hd, T, "cuda")
     x = torch.randn(B, T, H * hd, device="cuda").to(torch.bfloat16).requires_grad_(True)
     y = fused.rope(x, cos, sin, T, H, hd)
