@@ -102,10 +102,15 @@ int qeft_nearest_codes(const float* w_dense, int oc, int m, int g, int bits, con
 int qeft_optq_codes(double* w64, const double* u64, const float* scales, const float* zeros, int oc, int m,
                     int g, int bits, double* err_ws, uint8_t* codes, void* stream);
 
+#define QEFT_Y_F32 1
+#define QEFT_Y_ACCUMULATE 2
+
 /* ---- decode GEMV (kernels.py:87-157 matvec_structured/irregular/online) ----
  * y[n][o] = sum_i W_hat[o][i] * x[n][i] for n < n_cols (1..16), x/y row-major.
- * y is act_dtype, or fp32 when y_f32 != 0. Needs qeft_gemv_workspace_bytes() of
- * scratch (the x gather buffer of irregular / online-reorder layouts). */
+ * y_f32 is a flags word: QEFT_Y_F32 (bit 0) writes fp32 y instead of act_dtype;
+ * QEFT_Y_ACCUMULATE (bit 1) adds to y (y += W x, rounded once: a fused residual add).
+ * Needs qeft_gemv_workspace_bytes() of scratch (the x gather buffer of irregular /
+ * online-reorder layouts). */
 size_t qeft_gemv_workspace_bytes(const qeft_linear_t* layer, int n_cols);
 int qeft_gemv(const qeft_linear_t* layer, const void* x, int64_t ldx, void* y, int64_t ldy, int y_f32,
               int n_cols, void* workspace, size_t workspace_bytes, void* stream);

@@ -43,7 +43,8 @@ namespace {
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kU = 4;                 // 64-column steps per pipelined batch
-constexpr int kR = 4;                 // per-warp cp.async ring depth (batches)
+constexpr int kR = 4;                 // per-warp cp.async ring depth (batches); 3 when a batched x
+                                      // (N > 1) would otherwise cost the second CTA per SM
 constexpr int kXSmemMax = 32 * 1024;  // stage x in smem up to this size, else read via L1
 
 int num_sms() {
@@ -71,7 +72,7 @@ struct GemvArgs {
   const uint8_t* x;  // fast: original columns; else pre-gathered B200 order [n][m_pad + k_pad]
   int64_t ldx;       // elements
   int64_t ldy;
-  int y_f32;
+  int y_f32;  // bit 0: fp32 output; bit 1: accumulate (y += W x, e.g. a residual stream)
   int m, m_pad, k, k_pad, g, ng, n, n_rb;
   int gathered;
   int nsq;      // quantized 64-column steps (m_pad / 64)
@@ -83,10 +84,14 @@ struct GemvArgs {
 
 template <typename T>
 __device__ __forceinline__ void store_out(const GemvArgs& a, void* y, int n, int row, float v) {
-  if (a.y_f32)
-    ((float*)y)[(int64_t)n * a.ldy + row] = v;
-  else
-    ((T*)y)[(int64_t)n * a.ldy + row] = from_f32<T>(v);
+  const int64_t i = (int64_t)n * a.ldy + row;
+  if (a.y_f32 & 1) {
+    float* p = (float*)y + i;
+    *p = (a.y_f32 & 2) ? *p + v : v;
+  } else {
+    T* p = (T*)y + i;
+    *p = from_f32<T>((a.y_f32 & 2) ? to_f32<T>(*p) + v : v);  // one rounding of y + Wx
+  }
 }
 
 // global row-block -> (layer, layer-local row-block)
@@ -147,7 +152,7 @@ struct Ring {
   static constexpr int kSlot = kU * 512 + kSP * 128;   // bytes per warp per batch
 };
 
-template <int BITS, int NT, int GT, typename T, bool XS>
+template <int BITS, int NT, int GT, typename T, bool XS, int R = kR>
 __global__ void __launch_bounds__(kThreads, 2)
 gemv_kernel(const GemvArgs a) {
   // dynamic smem: [x (XS only): n x xs_ld][weak tiles: 2 x wbytes][rings: kWarps x kR x kSlot]
@@ -170,7 +175,7 @@ gemv_kernel(const GemvArgs a) {
   // per-(group, column) sums of x: the zero-point term of the fold, shared by every row
   float* xsum = reinterpret_cast<float*>(smem + (XS ? (size_t)a.n * a.xs_ld * sizeof(T) : 0));
   uint8_t* wsm = reinterpret_cast<uint8_t*>(xsum) + xsum_bytes(a.ng, NT);
-  uint8_t* ring = wsm + 2 * wbytes + (size_t)warp * kR * kSlot;
+  uint8_t* ring = wsm + 2 * wbytes + (size_t)warp * R * kSlot;
 
   auto rb_of = [&](int j) { return (int)blockIdx.x + j * (int)gridDim.x; };
 
@@ -312,7 +317,7 @@ gemv_kernel(const GemvArgs a) {
   int ij = 0, ib = 0;
   auto issue_next = [&](int t) {
     if (t < TB && !a.dbg) {
-      uint8_t* slot = ring + (t % kR) * kSlot;
+      uint8_t* slot = ring + (t % R) * kSlot;
       int rb;
       const int l = layer_of(a, rb_of(ij), rb);
       const int b0 = s_beg + ib * kU;
@@ -373,7 +378,7 @@ gemv_kernel(const GemvArgs a) {
     }
   };
   auto compute = [&](int t, int j, int b) {
-    const uint8_t* slot = ring + (t % kR) * kSlot;
+    const uint8_t* slot = ring + (t % R) * kSlot;
     const int rb = rb_of(j);
     const int b0 = s_beg + b * kU;
     if (b0 + kU <= s_end) {
@@ -447,7 +452,7 @@ gemv_kernel(const GemvArgs a) {
     fence_mbar_init();
   }
 #pragma unroll
-  for (int t = 0; t < kR - 1; ++t) issue_next(t);
+  for (int t = 0; t < R - 1; ++t) issue_next(t);
   // Programmatic dependent launch: the next layer may start streaming its weights
   // now; x (the previous kernel's output) and the trainable weak block are read
   // after the wait.
@@ -568,10 +573,10 @@ gemv_kernel(const GemvArgs a) {
   }
   int cj = 0, cb = 0;
   for (int t = 0; t < TB; ++t) {
-    cp_async_wait<kR - 2>();  // batch t has landed (this lane's copies)
+    cp_async_wait<R - 2>();  // batch t has landed (this lane's copies)
     __syncwarp();             // ... and every lane's (group params are shared)
     compute(t, cj, cb);
-    issue_next(t + kR - 1);   // refills the slot consumed at t - 1
+    issue_next(t + R - 1);   // refills the slot consumed at t - 1
     if (++cb == nb) {
       finish(cj);
       cb = 0;
@@ -580,31 +585,54 @@ gemv_kernel(const GemvArgs a) {
   }
 }
 
+template <int BITS, int NT, int GT, typename T, bool XS, int R>
+int launch_kernel(const GemvArgs& a, size_t smem, int per_sm, cudaStream_t st) {
+  auto kern = gemv_kernel<BITS, NT, GT, T, XS, R>;
+  static size_t max_dyn = 0;
+  if (!max_dyn) {  // all the dynamic smem the SM leaves next to this kernel's static smem
+    cudaFuncAttributes fa{};
+    QEFT_CUDA(cudaFuncGetAttributes(&fa, kern));
+    max_dyn = std::min<size_t>(227 * 1024 - fa.sharedSizeBytes, (size_t)env_int("QEFT_GEMV_MAXDYN", 227 * 1024));
+    QEFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_dyn));
+  }
+  QEFT_CHECK(smem <= max_dyn, QEFT_ERR_LAYOUT, "gemv: %zu B of shared memory (k_pad=%d, n=%d) too large", smem,
+             a.k_pad, a.n);
+  // persistent CTAs, equal row-block counts per CTA
+  const int slots = per_sm * num_sms();
+  const int per = (a.n_rb + slots - 1) / slots;
+  const int grid = (a.n_rb + per - 1) / per;
+  QEFT_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, a));
+  return 0;
+}
+
 template <int BITS, int NT, int GT, typename T>
 int launch(const GemvArgs& a0, cudaStream_t st) {
   GemvArgs a = a0;
   const size_t xs_bytes = (size_t)a.n * (a.m_pad + a.k_pad + 8) * sizeof(T);
   const size_t w_bytes = (size_t)2 * (a.k_pad / 64) * 2048;
-  const size_t ring_bytes = (size_t)kWarps * kR * Ring<GT>::kSlot;
-  const bool xs = xs_bytes <= (size_t)kXSmemMax;
+  const size_t fixed = xsum_bytes(a.ng, NT) + w_bytes;
+  const size_t ring4 = (size_t)kWarps * kR * Ring<GT>::kSlot, ring3 = (size_t)kWarps * 3 * Ring<GT>::kSlot;
+  static const size_t xs_max = (size_t)env_int("QEFT_GEMV_XSMAX", 200 * 1024);  // tuning
+  constexpr size_t kStatic = 9 * 1024;  // per-CTA static smem + reserve (what every launch so far fit)
+  auto fits2 = [&](size_t dyn) { return 2 * (dyn + kStatic) <= 227 * 1024; };
+  // x staged in smem whenever it fits; prefer two CTAs per SM (a 3-batch ring if that is what
+  // keeps the second CTA), else one CTA per SM with the whole x resident
+  const bool xs = xs_bytes <= xs_max && fixed + ring4 + xs_bytes + kStatic <= 227 * 1024;
   a.xs_ld = xs ? a.m_pad + a.k_pad + 8 : 0;  // 16 B skew between rows: conflict-free LDS.128
-  const size_t smem = (xs ? xs_bytes : 0) + xsum_bytes(a.ng, NT) + w_bytes + ring_bytes;
-  QEFT_CHECK(smem <= 200 * 1024, QEFT_ERR_LAYOUT, "gemv: k_pad=%d too large", a.k_pad);
-  // persistent CTAs: as many per SM as shared memory allows (<= 2: registers),
-  // equal row-block counts per CTA
-  int per_sm = smem * 2 + 2 * 9 * 1024 <= 227 * 1024 ? 2 : 1;
+  const size_t xb = xs ? xs_bytes : 0;
+  int per_sm = fits2(fixed + ring4 + xb) ? 2 : 1;
+  // (x of more than 8 columns never fits two CTAs: the 3-batch form exists for NT == 1 only)
+  const bool r3 = NT == 1 && per_sm == 1 && a.n > 1 && fits2(fixed + ring3 + xb);
+  if (r3) per_sm = 2;
   per_sm = std::min(per_sm, env_int("QEFT_GEMV_CPS", per_sm));
-  const int slots = per_sm * num_sms();
-  const int per = (a.n_rb + slots - 1) / slots;
-  const int grid = (a.n_rb + per - 1) / per;
-  auto kern = xs ? gemv_kernel<BITS, NT, GT, T, true> : gemv_kernel<BITS, NT, GT, T, false>;
-  static bool attr[2] = {false, false};
-  if (!attr[xs]) {
-    QEFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr[xs] = true;
+  if constexpr (NT == 1) {
+    if (r3) {
+      if (xs) return launch_kernel<BITS, NT, GT, T, true, 3>(a, fixed + ring3 + xb, per_sm, st);
+      return launch_kernel<BITS, NT, GT, T, false, 3>(a, fixed + ring3, per_sm, st);
+    }
   }
-  QEFT_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, a));
-  return 0;
+  if (xs) return launch_kernel<BITS, NT, GT, T, true, kR>(a, fixed + ring4 + xb, per_sm, st);
+  return launch_kernel<BITS, NT, GT, T, false, kR>(a, fixed + ring4, per_sm, st);
 }
 
 template <int BITS, typename T>

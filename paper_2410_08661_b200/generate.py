@@ -8,8 +8,9 @@ its matvec path. `KVDecoder` is the B200 form of the same greedy loop. Per token
   -> rotary at the token's position (qeft_rope)
   -> append k/v to the cache
   -> attention over the cache (torch SDPA, fp32 softmax inside the kernel)
-  -> o (qeft_gemv, irregular / online-reorder layouts gather x in-kernel) + residual
-  -> RMS-norm -> gate/up (one launch) -> SiLU*up (qeft_silu_mul_fwd) -> down + residual
+  -> o (qeft_gemv, irregular / online-reorder layouts gather x in-kernel), the residual add
+     fused into its epilogue (QEFT_Y_ACCUMULATE)
+  -> RMS-norm -> gate/up (one launch) -> SiLU*up (qeft_silu_mul_fwd) -> down, residual fused
 The final norm and the frozen dense head follow, then argmax. Semantics follow the reference
 engine's forward (model.py:323-407): one decode step at position p equals column p of a full
 causal forward. The same greedy token choice (np.argmax: first maximum) is kept.
@@ -80,7 +81,7 @@ class KVDecoder:
         cfg, B = self.cfg, self.B
         H, hd = cfg.n_heads, cfg.head_dim
         dyn = isinstance(pos, torch.Tensor)
-        x = F.embedding(tok, self.emb)  # (B, d)
+        x = F.embedding(tok, self.emb).contiguous()  # (B, d) residual stream, updated in place
         if dyn:
             cs, sn = self.cos.index_select(0, pos.view(1)), self.sin.index_select(0, pos.view(1))
             keep = (torch.arange(self.T, device=tok.device) <= pos).view(1, 1, 1, self.T)
@@ -107,7 +108,8 @@ class KVDecoder:
                 vc[:, :, pos:pos + 1] = v
                 o = F.scaled_dot_product_attention(q, kc[:, :, :pos + 1], vc[:, :, :pos + 1],
                                                    scale=1.0 / math.sqrt(hd))
-            x = x + blk.wo.dl.gemv(o.transpose(1, 2).reshape(B, H * hd))
+            x = x.contiguous()
+            blk.wo.dl.gemv(o.transpose(1, 2).reshape(B, H * hd), out=x, accumulate=True)  # x += Wo o
             b2 = fused.rms_norm(x, blk.gain2)
             if self.gu_fused[i]:
                 gt = torch.empty(B, blk.w_gate.oc, dtype=self.dt, device=x.device)
@@ -115,7 +117,7 @@ class KVDecoder:
                 decode.gemv_multi([blk.w_gate.dl, blk.w_up.dl], b2, [gt, up])
             else:
                 gt, up = blk.w_gate.dl.gemv(b2), blk.w_up.dl.gemv(b2)
-            x = x + blk.w_down.dl.gemv(fused.silu_mul(gt, up))
+            blk.w_down.dl.gemv(fused.silu_mul(gt, up), out=x, accumulate=True)  # x += Wdown f
         z = fused.rms_norm(x, self.model.final_gain)
         return (z @ self.head.t()).float()  # (B, V) fp32 logits
 

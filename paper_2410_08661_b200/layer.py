@@ -145,8 +145,9 @@ class DeviceLayer:
         return self.oc * row_bytes(self.m, self.bits) + 8 * self.oc * self.ng + 2 * self.oc * self.k
 
     # ------------------------------------------------------------------
-    def gemv(self, x, out=None, out_f32=False):
-        """y[n] = W_hat x[n] for x of shape (n, ic), n <= 16 (decode path)."""
+    def gemv(self, x, out=None, out_f32=False, accumulate=False):
+        """y[n] = W_hat x[n] for x of shape (n, ic), n <= 16 (decode path). With
+        accumulate=True, out += W_hat x in the kernel's epilogue (a fused residual add)."""
         import torch
         _lib.require_cuda(x, "x")
         if x.dim() != 2 or x.shape[1] != self.ic:
@@ -157,6 +158,8 @@ class DeviceLayer:
             x = x.contiguous()
         n = x.shape[0]
         if out is None:
+            if accumulate:
+                raise ShapeError("gemv: accumulate needs an output to add to")
             out = torch.empty((n, self.oc), dtype=torch.float32 if out_f32 else self.tdtype,
                               device=x.device)
         L = _lib.lib()
@@ -164,9 +167,9 @@ class DeviceLayer:
         ws = WORKSPACE.get(wsb, x.device)
         ldx = x.stride(0) if n > 1 else self.ic      # size-1 dims may carry any stride
         ldy = out.stride(0) if n > 1 else self.oc
-        _lib.check(L.qeft_gemv(self.cptr, _lib.ptr(x), ldx, _lib.ptr(out), ldy,
-                               1 if out.dtype == torch.float32 else 0, n, _lib.ptr(ws), ws.numel(),
-                               _lib.stream_ptr()), "gemv")
+        flags = (1 if out.dtype == torch.float32 else 0) | (2 if accumulate else 0)
+        _lib.check(L.qeft_gemv(self.cptr, _lib.ptr(x), ldx, _lib.ptr(out), ldy, flags, n, _lib.ptr(ws),
+                               ws.numel(), _lib.stream_ptr()), "gemv")
         return out
 
     def gemm_fwd(self, x, out=None):

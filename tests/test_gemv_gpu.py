@@ -275,3 +275,20 @@ def test_gemv_multi_matches_single_launches(B, n):
     gemv_multi(two, xb, outs)
     for a, b in zip(ref, outs):
         assert torch.equal(a, b)
+
+
+def test_gemv_accumulate_epilogue(B):
+    """QEFT_Y_ACCUMULATE: y += W x in the epilogue (one rounding), fp16 and fp32 outputs."""
+    import torch
+    from paper_2410_08661_b200.decode import random_layer
+    dl = random_layer(512, 1024, 64, 4, 128, "f16", seed=3)
+    for n in (1, 5):
+        x = torch.randn(n, 1024, device="cuda").half()
+        y0 = torch.randn(n, 512, device="cuda").half()
+        ref = y0.float() + dl.gemv(x, out_f32=True)
+        y = y0.clone()
+        dl.gemv(x, out=y, accumulate=True)
+        assert rel_err(y.float().cpu().numpy(), ref.cpu().numpy()) <= 1e-3
+        yf = y0.float().clone()
+        dl.gemv(x, out=yf, accumulate=True)
+        assert rel_err(yf.cpu().numpy(), ref.cpu().numpy()) <= 1e-6
