@@ -293,6 +293,28 @@ def run_b200(args):
     e2e = ws * bytes_step * args.steps / te / 1e9
 
     roof = kernel_roofline(torch, min(args.blocks, 32), peak, n, fuse=not args.no_fuse) if rank == 0 else []
+    # configs[1] is batch 1..16: the same stack at the other column counts (same layers, device
+    # time of 10 graph replays each; the headline value stays at --n-cols)
+    sweep = []
+    if rank == 0 and not args.no_sweep:
+        for nc in (1, 2, 4, 8, 16):
+            if nc == n:
+                continue
+            st2 = LinearStack(layers, n_cols=nc, groups=groups)
+            for _ in range(3):
+                st2.step()
+            torch.cuda.synchronize()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            for _ in range(10):
+                st2.step()
+            s1.record()
+            torch.cuda.synchronize()
+            sec = s0.elapsed_time(s1) / 1e3 / 10
+            gbs = st2.bytes_per_step() / sec / 1e9
+            sweep.append({"n_cols": nc, "value": gbs, "unit": "GB/s", "frac": gbs / peak,
+                          "ms_per_step": sec * 1e3})
+            del st2
     n_layers = len(layers)
     del stack, layers
     torch.cuda.empty_cache()
@@ -335,6 +357,7 @@ def run_b200(args):
             "cpu_baseline": cpu,
             "finetune": ft,
             "decode_step": ds,
+            "batch_sweep": sweep or None,
         }
         line["e2e"]["h2d_bytes_per_step"] = sum(2 * n * ic for ic in sorted({s[1] for s in BLOCK_SHAPES}))
         line["e2e"]["d2h_bytes_per_step"] = sum(2 * n * oc for oc, _ in BLOCK_SHAPES) * args.blocks
@@ -521,6 +544,7 @@ def main():
     ap.add_argument("--no-ft", action="store_true", help="skip the fine-tune step measurement")
     ap.add_argument("--no-fuse", action="store_true", help="one GEMV launch per layer (no q/k/v, gate/up grouping)")
     ap.add_argument("--no-dstep", action="store_true", help="skip the end-to-end decode step measurement")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the n_cols 1..16 sweep of the decode stack")
     ap.add_argument("--dstep-ctx", type=int, default=512)
     ap.add_argument("--ft-blocks", type=int, default=32)
     ap.add_argument("--ft-seq", type=int, default=2048)
