@@ -153,7 +153,7 @@ struct Ring {
 };
 
 template <int BITS, int NT, int GT, typename T, bool XS, int R = kR>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, (NT == 1 || !XS) ? 2 : 1)  // NT = 2, x resident: 1 CTA/SM anyway
 gemv_kernel(const GemvArgs a) {
   // dynamic smem: [x (XS only): n x xs_ld][weak tiles: 2 x wbytes][rings: kWarps x kR x kSlot]
   extern __shared__ __align__(128) uint8_t smem[];
