@@ -303,6 +303,18 @@ def gen_container():
         seq = np.concatenate([prompt, gen.tokens])[None, :-1]
         glog, _, _ = M.forward_batch(em, seq, want_cache=False)
         d[f"{reo}_prompt"], d[f"{reo}_gen_tokens"], d[f"{reo}_gen_logits"] = prompt, gen.tokens, glog
+        # weak-delta merging (merging.py): a 2-step tuned descendant, its delta (container kind 3)
+        # and the delta applied back onto the base
+        from qeft import merging
+        tc = tuning.TuneConfig(steps=2, lr=1e-3, batch=2, grad_accum=1, seq_len=32, seed=4, log_every=1)
+        tuned, _ = tuning.finetune(qm, ids, tc)
+        C.save_checkpoint(os.path.join(OUT, f"toy_{reo}_tuned.qeft"), tuned)
+        delta = merging.extract_delta(tuned, qm)
+        C.save_checkpoint(os.path.join(OUT, f"toy_{reo}.delta.qeft"), delta)
+        merged = merging.apply_to_quantized(qm, delta)
+        for name, q in merged.layer_items():
+            d[f"{reo}_merged_{name}"] = q.weak
+        d[f"{reo}_plan_digest"] = np.array(merging.plan_digest(qm))
     np.savez_compressed(os.path.join(OUT, "container.npz"), **d)
 
 

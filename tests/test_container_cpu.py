@@ -84,7 +84,7 @@ def test_container_errors():
     with pytest.raises(TruncatedFileError):  # trailing bytes after the last record
         C.loads(_reseal(data[:-4] + b"\x00"))
     body = bytearray(data[:-4])
-    body[6] = C.KIND_DELTA
+    body[6] = C.KIND_DENSE
     with pytest.raises(ContainerError):
         C.loads(_reseal(bytes(body)))
     body[6] = 9
