@@ -178,6 +178,12 @@ int qeft_weak_shadow(const float* w32, const qeft_shadow_desc_t* descs, int n_la
 int qeft_rmsnorm_fwd(const void* x, const float* gain, void* y, float* rstd, int rows, int C, int dt, void* stream);
 int qeft_rmsnorm_bwd(const void* dy, const void* x, const float* gain, const float* rstd, const void* dres,
                      void* dx, int rows, int C, int dt, void* stream);
+/* Decode step: q_out = rope(q), k_cache[b][h][pos] = rope(k), v_cache[b][h][pos] = v for q/k/v
+ * of shape (B, H*hd) at the position *pos (a device int64, so one CUDA graph serves every
+ * step); caches (B, H, T_cache, hd); cos/sin tables [T_cache][hd/2]. */
+int qeft_rope_kv(const void* q, const void* k, const void* v, void* q_out, void* k_cache, void* v_cache,
+                 const float* cos_t, const float* sin_t, const int64_t* pos, int B, int H, int hd, int T_cache, int dt,
+                 void* stream);
 int qeft_rope(const void* in, void* out, const float* cos_t, const float* sin_t, int64_t rows, int T, int H,
               int hd, int inverse, int dt, void* stream);
 int qeft_silu_mul_fwd(const void* g, const void* u, void* f, int64_t n, int dt, void* stream);

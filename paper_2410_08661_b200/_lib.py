@@ -65,6 +65,7 @@ SIGNATURES = {
     "qeft_rmsnorm_fwd": (_I, [_VP, _VP, _VP, _VP, _I, _I, _I, _VP]),
     "qeft_rmsnorm_bwd": (_I, [_VP, _VP, _VP, _VP, _VP, _VP, _I, _I, _I, _VP]),
     "qeft_rope": (_I, [_VP, _VP, _VP, _VP, _I64, _I, _I, _I, _I, _I, _VP]),
+    "qeft_rope_kv": (_I, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I, _I, _I, _I, _I, _VP]),
     "qeft_silu_mul_fwd": (_I, [_VP, _VP, _VP, _I64, _I, _VP]),
     "qeft_silu_mul_bwd": (_I, [_VP, _VP, _VP, _VP, _VP, _I64, _I, _VP]),
     "qeft_last_error": (ctypes.c_char_p, []),

@@ -163,6 +163,12 @@ int qeft_rmsnorm_bwd(const void* dy, const void* x, const float* gain, const flo
   return rmsnorm_bwd(dy, x, gain, rstd, dres, dx, rows, C, dt, ST(s));
 }
 
+int qeft_rope_kv(const void* q, const void* k, const void* v, void* q_out, void* k_cache, void* v_cache,
+                 const float* cos_t, const float* sin_t, const int64_t* pos, int B, int H, int hd, int T_cache, int dt,
+                 void* s) {
+  return rope_kv(q, k, v, q_out, k_cache, v_cache, cos_t, sin_t, pos, B, H, hd, T_cache, dt, ST(s));
+}
+
 int qeft_rope(const void* in, void* out, const float* cosv, const float* sinv, int64_t rows, int T, int H, int hd,
               int inverse, int dt, void* s) {
   return rope(in, out, cosv, sinv, rows, T, H, hd, inverse, dt, ST(s));

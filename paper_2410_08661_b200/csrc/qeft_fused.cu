@@ -154,6 +154,35 @@ __global__ void rope_kernel(const T* __restrict__ in, T* __restrict__ out, const
   }
 }
 
+// One decode step's rotary + KV-cache append (model.py:249-259, 372-380 at one position):
+// q_out = rot(q), k_cache[b][h][pos] = rot(k), v_cache[b][h][pos] = v. q, k, v are (B, H*hd)
+// GEMV outputs; caches (B, H, T_cache, hd). pos is read on device (one CUDA graph per step).
+template <typename T>
+__global__ void rope_kv_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
+                               T* __restrict__ q_out, T* __restrict__ kc, T* __restrict__ vc,
+                               const float* __restrict__ cosv, const float* __restrict__ sinv,
+                               const int64_t* __restrict__ pos_dev, int H, int hd, int T_cache) {
+  const int b = blockIdx.x, half = hd >> 1;
+  const int64_t pos = *pos_dev;
+  const float* cr = cosv + pos * half;
+  const float* sr = sinv + pos * half;
+  for (int e = threadIdx.x; e < H * half; e += blockDim.x) {
+    const int h = e / half, j = e - h * half;
+    const int64_t src = ((int64_t)b * H + h) * hd;
+    const int64_t dst = (((int64_t)b * H + h) * T_cache + pos) * hd;
+    const float c = cr[j], s = sr[j];
+    float a = to_f32<T>(q[src + j]), bb = to_f32<T>(q[src + j + half]);
+    q_out[src + j] = from_f32<T>(a * c - bb * s);
+    q_out[src + j + half] = from_f32<T>(a * s + bb * c);
+    a = to_f32<T>(k[src + j]);
+    bb = to_f32<T>(k[src + j + half]);
+    kc[dst + j] = from_f32<T>(a * c - bb * s);
+    kc[dst + j + half] = from_f32<T>(a * s + bb * c);
+    vc[dst + j] = v[src + j];
+    vc[dst + j + half] = v[src + j + half];
+  }
+}
+
 // f = silu(g) * u (SwiGLU, model.py:389-391) and its backward
 template <typename T>
 __global__ void silu_mul_fwd_kernel(const T* __restrict__ g, const T* __restrict__ u, T* __restrict__ f, int64_t n) {
@@ -230,6 +259,23 @@ int rmsnorm_bwd(const void* dy, const void* x, const float* gain, const float* r
   else
     rmsnorm_bwd_kernel<__half><<<rows, thr, 0, st>>>((const __half*)dy, (const __half*)x, gain, rstd,
                                                     (const __half*)dres, (__half*)dx, C);
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int rope_kv(const void* q, const void* k, const void* v, void* q_out, void* kc, void* vc, const float* cosv,
+            const float* sinv, const int64_t* pos_dev, int B, int H, int hd, int T_cache, int dt, cudaStream_t st) {
+  QEFT_CHECK(hd % 2 == 0 && hd > 0 && B >= 1 && H >= 1 && T_cache >= 1, QEFT_ERR_SHAPE,
+             "rope_kv: B=%d H=%d hd=%d T=%d", B, H, hd, T_cache);
+  const int thr = std::min(512, std::max(32, H * hd / 2));
+  if (dt == QEFT_BF16)
+    rope_kv_kernel<__nv_bfloat16><<<B, thr, 0, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+                                                     (const __nv_bfloat16*)v, (__nv_bfloat16*)q_out,
+                                                     (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, cosv, sinv, pos_dev,
+                                                     H, hd, T_cache);
+  else
+    rope_kv_kernel<__half><<<B, thr, 0, st>>>((const __half*)q, (const __half*)k, (const __half*)v, (__half*)q_out,
+                                              (__half*)kc, (__half*)vc, cosv, sinv, pos_dev, H, hd, T_cache);
   QEFT_CUDA(cudaGetLastError());
   return 0;
 }

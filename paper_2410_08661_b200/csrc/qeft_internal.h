@@ -73,6 +73,8 @@ int weak_shadow(const float* w32, const qeft_shadow_desc_t* d, int n_layers, int
 int rmsnorm_fwd(const void* x, const float* gain, void* y, float* rstd, int rows, int C, int dt, cudaStream_t st);
 int rmsnorm_bwd(const void* dy, const void* x, const float* gain, const float* rstd, const void* dres, void* dx,
                 int rows, int C, int dt, cudaStream_t st);
+int rope_kv(const void* q, const void* k, const void* v, void* q_out, void* kc, void* vc, const float* cosv,
+            const float* sinv, const int64_t* pos_dev, int B, int H, int hd, int T_cache, int dt, cudaStream_t st);
 int rope(const void* in, void* out, const float* cosv, const float* sinv, int64_t rows, int T, int H, int hd,
          int inverse, int dt, cudaStream_t st);
 int silu_mul_fwd(const void* g, const void* u, void* f, int64_t n, int dt, cudaStream_t st);

@@ -98,3 +98,14 @@ def rope(x, cos, sin, T, H, hd):
 
 def silu_mul(g, u):
     return _SiluMul.apply(g, u)
+
+
+def rope_kv(q, k, v, q_out, k_cache, v_cache, cos, sin, pos_dev, H, hd):
+    """Decode step (no autograd): q_out = rope(q); k_cache/v_cache[:, :, *pos_dev] = rope(k), v.
+    q/k/v (B, H*hd); caches (B, H, T, hd); pos_dev a device int64 scalar."""
+    B, T = q.shape[0], k_cache.shape[2]
+    _lib.check(_lib.lib().qeft_rope_kv(q.data_ptr(), k.data_ptr(), v.data_ptr(), q_out.data_ptr(),
+                                       k_cache.data_ptr(), v_cache.data_ptr(), cos.data_ptr(), sin.data_ptr(),
+                                       pos_dev.data_ptr(), B, H, hd, T, _TDT[q.dtype], _lib.stream_ptr()),
+               "rope_kv")
+    return q_out

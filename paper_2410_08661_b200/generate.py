@@ -5,8 +5,7 @@ each new token recomputes the whole prefix, every linear layer going column by c
 its matvec path. `KVDecoder` is the B200 form of the same greedy loop. Per token and block it runs:
   RMS-norm (qeft_rmsnorm_fwd)
   -> q/k/v: one qeft_gemv_multi launch when the three share geometry, else per-layer qeft_gemv
-  -> rotary at the token's position (qeft_rope)
-  -> append k/v to the cache
+  -> rotary on q/k at the token's position + k/v appended to the cache (one qeft_rope_kv)
   -> attention over the cache (torch SDPA, fp32 softmax inside the kernel)
   -> o (qeft_gemv, irregular / online-reorder layouts gather x in-kernel), the residual add
      fused into its epilogue (QEFT_Y_ACCUMULATE)
@@ -83,10 +82,7 @@ class KVDecoder:
         dyn = isinstance(pos, torch.Tensor)
         x = F.embedding(tok, self.emb).contiguous()  # (B, d) residual stream, updated in place
         if dyn:
-            cs, sn = self.cos.index_select(0, pos.view(1)), self.sin.index_select(0, pos.view(1))
             keep = (torch.arange(self.T, device=tok.device) <= pos).view(1, 1, 1, self.T)
-        else:
-            cs, sn = self.cos[pos:pos + 1], self.sin[pos:pos + 1]
         for i, blk in enumerate(self.model.blocks):
             a = fused.rms_norm(x, blk.gain1)
             if self.qkv_fused[i]:
@@ -95,17 +91,13 @@ class KVDecoder:
                 decode.gemv_multi([blk.wq.dl, blk.wk.dl, blk.wv.dl], a, [q, k, v])
             else:
                 q, k, v = blk.wq.dl.gemv(a), blk.wk.dl.gemv(a), blk.wv.dl.gemv(a)
-            q = fused.rope(q, cs, sn, 1, H, hd).view(B, 1, H, hd).transpose(1, 2)
-            k = fused.rope(k, cs, sn, 1, H, hd).view(B, H, 1, hd)
-            v = v.view(B, H, 1, hd)
             kc, vc = self.k_cache[i], self.v_cache[i]
+            # rotary on q and k + the cache append at the device position, one kernel
+            qr = fused.rope_kv(q, k, v, torch.empty_like(q), kc, vc, self.cos, self.sin, self.pos_dev, H, hd)
+            q = qr.view(B, H, 1, hd)
             if dyn:
-                kc.index_copy_(2, pos.view(1), k)
-                vc.index_copy_(2, pos.view(1), v)
                 o = F.scaled_dot_product_attention(q, kc, vc, attn_mask=keep, scale=1.0 / math.sqrt(hd))
             else:
-                kc[:, :, pos:pos + 1] = k
-                vc[:, :, pos:pos + 1] = v
                 o = F.scaled_dot_product_attention(q, kc[:, :, :pos + 1], vc[:, :, :pos + 1],
                                                    scale=1.0 / math.sqrt(hd))
             x = x.contiguous()
@@ -127,10 +119,10 @@ class KVDecoder:
         if not 0 <= pos < self.T:
             raise ShapeError(f"position {pos} outside the cache (max_seq {self.T})")
         tok = torch.as_tensor(tok, dtype=torch.int64).view(self.B)
+        self.pos_dev.fill_(pos)  # read on device by the rotary + cache-append kernel
         if not self.capture:
             return self._step(tok.to(self.tok_dev.device), pos)
         self.tok_dev.copy_(tok, non_blocking=True)
-        self.pos_dev.fill_(pos)
         if self.graph is None:
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
