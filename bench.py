@@ -318,7 +318,7 @@ def run_b200(args):
     n_layers = len(layers)
     del stack, layers
     torch.cuda.empty_cache()
-    ds = None if (args.no_dstep or rank != 0) else decode_step_bench(args, torch)
+    ds = None if (args.no_dstep or rank != 0) else decode_step_bench(args, torch, dev)
     torch.cuda.empty_cache()
     ft = None if args.no_ft else finetune_bench(args, ws, rank, dev, torch)
     line = None
@@ -367,7 +367,7 @@ def run_b200(args):
     return line
 
 
-def decode_step_bench(args, torch):
+def decode_step_bench(args, torch, dev):
     """Whole decode step around the GEMV: 7B-shaped QEFTDecoder, batch 1,
     KV cache at `--dstep-ctx` tokens. One CUDA graph per step covers norms, q/k/v and
     gate/up as fused GEMV launches, rotary, the cache write, attention, o/down, SiLU*mul, the
@@ -379,18 +379,21 @@ def decode_step_bench(args, torch):
     model = QEFTDecoder.synthetic(LLAMA2_7B, k=128, bits=4, g=128, act_dtype="f16", compute_dtype="f16")
     for p in model.parameters():
         p.requires_grad_(False)
-    ctx, steps = args.dstep_ctx, 32
+    ctx, steps = args.dstep_ctx, 128
     dec = KVDecoder(model, max_seq=ctx + steps + 1, capture=True)
     tok = torch.tensor([1])
     for p in range(ctx):  # fill the cache (untimed)
         dec.step(tok, p)
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-    e0.record()
-    for i in range(steps):
-        dec.step(tok, ctx + i)
-    e1.record()
-    torch.cuda.synchronize()
+    # this latency-bound step is clock-sensitive: after an idle second the GPU can stay ~8%
+    # slower for it (scripts/dstep_gap.py), so the clocks it ran at go into the record
+    with ClockSampler(dev) as clk:
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        for i in range(steps):
+            dec.step(tok, ctx + i)
+        e1.record()
+        torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     del dec, model
     return {"metric": "QEFT greedy decode tokens/s (batch 1)", "value": 1e3 / ms, "unit": "tokens/s",
@@ -398,7 +401,7 @@ def decode_step_bench(args, torch):
             "config": {"workload": "LLaMA-2-7B-shaped QEFT decoder (4-bit g128 k=128, 32 blocks, fp16), "
                                    "KV cache, one CUDA graph per step",
                        "context": ctx, "batch": 1},
-            "data": "synthetic", "dtype": "f16"}
+            "clocks": clk.summary(), "data": "synthetic", "dtype": "f16"}
 
 
 def finetune_bench(args, ws, rank, local, torch):
