@@ -833,7 +833,10 @@ int dispatch_gemm(const qeft_linear_t* L, int T_, const CUtensorMap& m0, const C
     return e ? atoi(e) : 0;
   }();
   const bool big = T_ > 128;
-  const bool pair = T_ > 256 && nsub_env != 1;
+  // paired sub-tiles halve dequant work per FLOP, but when even twice the items of single
+  // sub-tiles fit one wave (few m-blocks, short T: 13B T=512), parallelism wins
+  const int pair_items = a.n_mblk * ((T_ + 511) / 512);
+  const bool pair = T_ > 256 && nsub_env != 1 && 2 * pair_items > num_sms();
   const int BN = big ? 256 : 128;
   a.n_nblk = (T_ + BN * (pair ? 2 : 1) - 1) / (BN * (pair ? 2 : 1));
   // weak block as a 4-D tensor {64 columns, 16 rows, k_pad/64 tiles, row-blocks} of the
