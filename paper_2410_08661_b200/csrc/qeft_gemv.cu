@@ -622,7 +622,7 @@ int launch(const GemvArgs& a0, cudaStream_t st) {
   const size_t xb = xs ? xs_bytes : 0;
   int per_sm = fits2(fixed + ring4 + xb) ? 2 : 1;
   // (x of more than 8 columns never fits two CTAs: the 3-batch form exists for NT == 1 only)
-  const bool r3 = NT == 1 && per_sm == 1 && a.n > 1 && fits2(fixed + ring3 + xb);
+  const bool r3 = NT == 1 && per_sm == 1 && fits2(fixed + ring3 + xb);
   if (r3) per_sm = 2;
   per_sm = std::min(per_sm, env_int("QEFT_GEMV_CPS", per_sm));
   if constexpr (NT == 1) {
