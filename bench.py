@@ -401,7 +401,11 @@ def decode_step_bench(args, torch, dev):
             "config": {"workload": "LLaMA-2-7B-shaped QEFT decoder (4-bit g128 k=128, 32 blocks, fp16), "
                                    "KV cache, one CUDA graph per step",
                        "context": ctx, "batch": 1},
-            "clocks": clk.summary(), "data": "synthetic", "dtype": "f16"}
+            "clocks": clk.summary(), "data": "synthetic", "dtype": "f16",
+            # the paper's generation speed for this workload (QEFT 7B, k=128, 4-bit
+            # g=128, batch 1) -- on an A100 80GB, so context, not a same-box ratio
+            "vs_baseline": 1e3 / ms / 146.0,
+            "baseline": {"value": 146.0, "unit": "tokens/s", "hardware": "A100 80GB", "source": "PAPER.md:227-228"}}
 
 
 def finetune_bench(args, ws, rank, local, torch):
