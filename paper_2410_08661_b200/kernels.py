@@ -7,7 +7,8 @@ Same names and contracts as pkg/src/qeft/kernels.py:38-186:
 Every path runs the B200 decode GEMV (libqeft_b200 `qeft_gemv`); the layout
 variants differ only in the colmap gather the kernel applies while staging x.
 Inputs/outputs are host numpy float32 like the reference; the device copy of
-the layer is cached on the record (QuantizedLinear.device()).
+the layer comes from layer.device_layer (cached per record, ours or the
+reference's own class, with the weak block re-synced from q.weak).
 """
 
 from __future__ import annotations
@@ -52,9 +53,10 @@ def analytic_fmas(q) -> int:
 
 
 def b200_bytes(q, n_cols: int = 1) -> int:
-    """Algorithmic HBM bytes of one B200 GEMV (fp16 params/weak, fp16 x and y)."""
+    """Algorithmic HBM bytes of one B200 GEMV: codes + fp16 (scale, zero)
+    + fp16 weak + fp16 x and y."""
     from .packing import row_bytes
-    return (q.oc * row_bytes(q.m, q.bits) + 8 * q.oc * q.n_groups + 2 * q.oc * q.k
+    return (q.oc * row_bytes(q.m, q.bits) + 4 * q.oc * q.n_groups + 2 * q.oc * q.k
             + 2 * n_cols * (q.ic + q.oc))
 
 
@@ -68,16 +70,21 @@ def _bump(stats, q, t0, path, n=1):
 def _run(q, xs: np.ndarray, perm=None) -> np.ndarray:
     """Columns of xs (ic, N) through the GEMV in chunks of 16; returns (oc, N) fp32."""
     import torch
-    dl = q.device("f16")
+    from .layer import device_layer
+    dl = device_layer(q, "f16")
     if perm is not None:
         # matvec_online_reorder with an explicit permutation: a throwaway view
         # of the layer whose colmap composes the permutation (kernels.py:115-126)
         dl = _with_perm(q, dl, perm)
-    xt = torch.from_numpy(np.ascontiguousarray(xs.T, np.float32)).cuda().to(torch.float16)
+    # fp16 operands: scale x by an exact power of two so max|x| lands in [1, 2) (no overflow
+    # past 65504, full fp16 precision for tiny inputs), divided back out of the fp32 result
+    from .tuning import _pow2_scale
+    sc = _pow2_scale(xs)
+    xt = torch.from_numpy(np.ascontiguousarray(xs.T * np.float32(sc), np.float32)).cuda().to(torch.float16)
     out = torch.empty((xt.shape[0], q.oc), dtype=torch.float32, device="cuda")
     for s in range(0, xt.shape[0], 16):
         dl.gemv(xt[s:s + 16], out=out[s:s + 16])
-    return out.cpu().numpy().T
+    return (out.cpu().numpy().T / np.float32(sc)).astype(np.float32)
 
 
 def _with_perm(q, dl, perm):
@@ -132,12 +139,13 @@ def matvec_online_reorder(q, x_original, perm, stats: KernelStats | None = None)
 
 
 def matvec_reference(q, x) -> np.ndarray:
-    """Dense path: the device-dequantized matrix times x in fp64 on the GPU."""
+    """Dense path: the device-dequantized matrix times x in fp64 on the GPU. The device
+    dequant writes column colmap[j] = input_perm[qpos[j]], i.e. W in ORIGINAL input
+    coordinates, so x is used as given (online layouts included)."""
     import torch
+    from .layer import device_layer
     x = np.asarray(x, dtype=np.float64)
-    if q.input_perm is not None:
-        x = x[q.input_perm]
-    w = q.device("f16").dequant_full().double()
+    w = device_layer(q, "f16").dequant_full().double()
     return (w @ torch.from_numpy(x).cuda()).cpu().numpy()
 
 

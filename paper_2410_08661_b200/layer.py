@@ -3,7 +3,7 @@ calls into the CUDA library (GEMV / GEMM / dequant).
 
 HBM layout of one layer (all on one GPU; see csrc/qeft_common.cuh):
   qweight  uint8   (oc_pad/16) row-blocks x K-tiles of 512 B (4-bit) / 768 B (3-bit)
-  sz       dtype   (scale, zero) pairs [oc_pad/16][ng][16][2]
+  sz       fp32    (scale, zero) pairs [oc_pad/16][ng][16][2] (the reference's storage precision)
   weak16   dtype   [oc_pad][k_pad]  (the trainable block's kernel shadow)
   colmap   int32   [m_pad + k_pad]  B200 K position -> input column (-1 padding)
   weak32   fp32    [oc][k]          trainable master (a view into the DP bucket
@@ -86,23 +86,31 @@ class DeviceLayer:
     def device(self):
         return self.qweight.device
 
-    def stale(self, q) -> bool:
-        return self.source_id != _source_id(q)
-
     # ------------------------------------------------------------------
     @classmethod
     def from_quantized(cls, q, dtype="f16", device="cuda"):
-        """Upload + repack a QuantizedLinear (reference record) on the GPU."""
+        """Upload + repack a QuantizedLinear (ours or the reference's record) on `device`;
+        the repack kernels run on that device's current stream."""
+        import torch
+        device = torch.device(device)
+        if device.index is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        with torch.cuda.device(device):
+            return cls._from_quantized(q, dtype, device)
+
+    @classmethod
+    def _from_quantized(cls, q, dtype, device):
         import torch
         from .packing import to_tiles
         oc, ic, k, bits, g = q.oc, q.ic, q.k, q.bits, q.g
         m = ic - k
         m_pad, k_pad = _pad(m, 128), _pad(k, 64)
-        qpos = q.quant_positions() if hasattr(q, "quant_positions") else None
         widx = np.asarray(q.weak_indices, np.int64)
         p = np.arange(ic) if q.input_perm is None else np.asarray(q.input_perm, np.int64)
         colmap = np.full(m_pad + k_pad, -1, np.int32)
-        colmap[:m] = p[qpos]
+        keep = np.ones(ic, dtype=bool)
+        keep[np.asarray(q.weak_indices, np.int64)] = False
+        colmap[:m] = p[np.flatnonzero(keep)]
         colmap[m_pad:m_pad + k] = p[widx]
         fast = (q.input_perm is None and q.layout == "structured" and m % 8 == 0 and ic % 8 == 0)
         qweight = to_tiles(q.packed, oc, m, bits, device=device)
@@ -139,10 +147,10 @@ class DeviceLayer:
         return out
 
     def weight_bytes(self) -> int:
-        """Algorithmic HBM bytes one GEMV must read (unpadded): codes + fp32
-        (scale, zero) (the reference's analytic_bytes, kernels.py:54-58) + fp16 weak."""
+        """Algorithmic HBM bytes one GEMV must read: codes +
+        fp16 (scale, zero) pairs (4 B per row and group) + fp16 weak block."""
         from .packing import row_bytes
-        return self.oc * row_bytes(self.m, self.bits) + 8 * self.oc * self.ng + 2 * self.oc * self.k
+        return self.oc * row_bytes(self.m, self.bits) + 4 * self.oc * self.ng + 2 * self.oc * self.k
 
     # ------------------------------------------------------------------
     def gemv(self, x, out=None, out_f32=False, accumulate=False):
@@ -262,7 +270,58 @@ class DeviceLayer:
 
 
 def _source_id(q):
-    """Identity of the host record contents the device copy was built from."""
-    w = q.weak
-    return (id(q), q.packed.__hash__() if isinstance(q.packed, (bytes, bytearray)) else id(q.packed),
-            w.ctypes.data if isinstance(w, np.ndarray) else id(w))
+    """Identity of the frozen parts of a host record the device copy was built from: the
+    packed codes, the (scale, zero) arrays, the weak column set and the input permutation.
+    The trainable weak block is NOT part of it: `device_layer` re-syncs it by content."""
+    perm = getattr(q, "input_perm", None)
+    return (id(q.packed), id(q.scales), id(q.zeros), q.layout,
+            np.asarray(q.weak_indices, np.int64).tobytes(),
+            None if perm is None else np.asarray(perm, np.int64).tobytes())
+
+
+class _DeviceCache:
+    """Device copies of host QuantizedLinear records, keyed by the record itself.
+
+    The reference's records (pkg/src/qeft/quantizer.py:42-57) are plain dataclasses with no
+    room for a device handle, and its fine-tune loop updates `q.weak` IN PLACE between steps
+    (tuning.py:159 adam_step, 234-236). So the cache lives here, not on the record: an entry
+    is dropped when its record is garbage collected (weakref finalizer), rebuilt when a frozen
+    field is replaced, and its weak block is re-uploaded whenever the host `q.weak` bytes
+    differ from the last upload (a memcmp of oc x k floats per call -- the reference itself
+    reads q.weak live on every call)."""
+
+    def __init__(self):
+        self.entries = {}  # (id(record), dtype, device) -> [weakref, source_id, weak snapshot, DeviceLayer]
+
+    def get(self, q, dtype="f16", device=None):
+        import torch
+        import weakref
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        key = (id(q), dtype, str(dev))
+        e = self.entries.get(key)
+        sid = _source_id(q)
+        if e is None or e[0]() is not q or e[1] != sid:
+            with torch.cuda.device(dev):
+                dl = DeviceLayer.from_quantized(q, dtype=dtype, device=dev)
+            try:
+                ref = weakref.ref(q, lambda _r, k=key: self.entries.pop(k, None))
+            except TypeError:  # records without weakref support stay cached until replaced
+                ref = (lambda obj=q: obj)
+            e = [ref, sid, np.array(q.weak, np.float32, copy=True), dl]
+            self.entries[key] = e
+        elif q.k and not np.array_equal(e[2], q.weak):
+            dl = e[3]
+            dl.weak32.copy_(torch.from_numpy(np.ascontiguousarray(q.weak, np.float32)))
+            with torch.cuda.device(dev):
+                dl.refresh_weak16()
+            e[2] = np.array(q.weak, np.float32, copy=True)
+        return e[3]
+
+
+DEVICE_CACHE = _DeviceCache()
+
+
+def device_layer(q, dtype: str = "f16", device=None) -> DeviceLayer:
+    """The B200 tile-layout copy of a host QuantizedLinear (ours or the reference's own
+    record class), cached per (record, dtype, device) with its weak block kept in sync."""
+    return DEVICE_CACHE.get(q, dtype, device)

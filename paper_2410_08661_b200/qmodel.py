@@ -83,13 +83,31 @@ class QuantizedModel:
                 yield f"b{i}.{nm}", b.layers[nm]
 
     def copy(self) -> "QuantizedModel":
-        # device copies (QuantizedLinear.device() caches) are rebuilt, never deep-copied
-        stash = []
-        for _, q in self.layer_items():
-            keys = [k for k in vars(q) if k.startswith("_b200_")]
-            stash.append((q, {k: vars(q).pop(k) for k in keys}))
-        try:
-            return copy.deepcopy(self)
-        finally:
-            for q, saved in stash:
-                vars(q).update(saved)
+        # device copies live in layer.DEVICE_CACHE, keyed by record: the copy gets its own
+        return copy.deepcopy(self)
+
+
+class QuantLinearInferOp:
+    """Frozen quantized linear (qmodel.py:162-185), the reference's default op for
+    quant_engine / quantized_perplexity (qmodel.py:206-224). The reference dequantizes once
+    and multiplies dense fp32; here the layer is repacked once into the B200 layout
+    (layer.device_layer) and every call runs the fused kernels: the decode GEMV for <= 16
+    activation columns, the tcgen05 GEMM above. backward returns (dX, None): no weight grad."""
+
+    def __init__(self, name: str, q):
+        from .layer import device_layer
+        self.name = name
+        self.q = q
+        self.oc, self.ic = q.oc, q.ic
+        device_layer(q, "f16")  # build the device copy now (the reference's dequant-once)
+
+    def apply(self, x2d):
+        from .tuning import qlinear_forward_train
+        return qlinear_forward_train(self.q, x2d)[0]
+
+    def forward_train(self, x2d):
+        return self.apply(x2d), None
+
+    def backward(self, state, dy2d, need_weight_grad=True):
+        from .tuning import dgrad_host
+        return dgrad_host(self.q, dy2d), None

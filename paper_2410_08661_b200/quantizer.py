@@ -95,14 +95,10 @@ class QuantizedLinear:
 
     # --- B200 device copy -------------------------------------------------
     def device(self, dtype="f16"):
-        """The B200 tile-layout copy on the current CUDA device (cached)."""
-        from .layer import DeviceLayer
-        key = "_b200_" + dtype
-        dl = getattr(self, key, None)
-        if dl is None or dl.stale(self):
-            dl = DeviceLayer.from_quantized(self, dtype=dtype)
-            object.__setattr__(self, key, dl)
-        return dl
+        """The B200 tile-layout copy on the current CUDA device (layer.device_layer: cached
+        per record, weak block re-synced from self.weak when it changes)."""
+        from .layer import device_layer
+        return device_layer(self, dtype)
 
 
 # ---------------------------------------------------------------------------

@@ -28,6 +28,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .errors import DivergenceError, ShapeError
+from .layer import device_layer
 from .optim import AdamState, adam_step  # noqa: F401  (reference names)
 
 
@@ -76,11 +77,24 @@ def qlinear_forward_train(q, x, *, w_hat_dense=None):
     state = TrainableLayerState(x_weak=np.ascontiguousarray(xs[q.weak_indices]), n_cols=T)
     if T == 0:
         return np.zeros((q.oc, 0), np.float32), state
-    dl = q.device("f16")
+    dl = device_layer(q, "f16")
     s = _pow2_scale(x)
     xt = _to_dev(x, s)
     y = dl.gemm_fwd(xt) if T > 16 else dl.gemv(xt, out_f32=True)
     return (y.float().cpu().numpy().T / np.float32(s)).astype(np.float32), state
+
+
+def dgrad_host(q, dy):
+    """dX = W_hat_full^T @ dY (un-permuted for online layers) through the tcgen05 dgrad GEMM;
+    dy (OC, T) f32 host -> (IC, T) f32 host. Also the frozen op's backward (qmodel.py:177-183)."""
+    dy = np.asarray(dy, dtype=np.float32)
+    t = dy.shape[1]
+    if t == 0:
+        return np.zeros((q.ic, 0), np.float32)
+    dl = device_layer(q, "f16")
+    sd = _pow2_scale(dy)
+    dx = dl.gemm_dgrad(_to_dev(dy, sd)).float().cpu().numpy().T / np.float32(sd)
+    return np.ascontiguousarray(dx, np.float32)
 
 
 def qlinear_backward(state: TrainableLayerState, dy, q, *, w_hat_dense=None,
@@ -96,7 +110,7 @@ def qlinear_backward(state: TrainableLayerState, dy, q, *, w_hat_dense=None,
                                   saved_elems=q.k * t, full_elems=q.ic * t))
     if t == 0:
         return np.zeros((q.ic, 0), np.float32), np.zeros((q.oc, q.k), np.float32)
-    dl = q.device("f16")
+    dl = device_layer(q, "f16")
     sd = _pow2_scale(dy)
     dyt = _to_dev(dy, sd)
     dx = dl.gemm_dgrad(dyt).float().cpu().numpy().T / np.float32(sd)
