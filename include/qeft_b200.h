@@ -54,6 +54,8 @@ typedef struct qeft_linear {
   const void* sz;        /* fp32 (scale, zero) pairs [oc_pad/16][ng][16][2] */
   const void* weak16;    /* [oc_pad][k_pad] */
   const int32_t* colmap; /* [m_pad + k_pad]: B200 K position -> input column, -1 pad */
+  const void* sz16;      /* decode-GEMV copy of (scale, zero): fp16 pairs [oc_pad/16][ng16][8][2],
+                            ng16 = ceil(m_pad / g); see qeft_pack_sz16. NULL: generic GEMV path */
 } qeft_linear_t;
 
 /* ---- format conversion (packing.py:24-72, quantizer.py:42-100) ---- */
@@ -70,6 +72,11 @@ int qeft_repack_to_ref(const void* qweight, int oc, int m, int bits, uint8_t* re
 /* fp32 scales/zeros [oc][ng] (quantizer.py:50-51) -> fp32 (scale, zero) pairs in the
  * row-block-major sz layout (the reference's storage precision, 8 B per group). */
 int qeft_pack_sz(const float* scales, const float* zeros, int oc, int ng, void* sz, void* stream);
+/* fp32 scales/zeros [oc][ng] -> the decode GEMV's fp16 (scale, zero) copy: half2 pairs
+ * [oc_pad/16][ng16][8][2] (rows r and r+8 adjacent, 64 B per row-block and group, zero
+ * padded to ng16 = ceil(roundup(m,128)/g) groups). qeft_sz16_bytes() gives its size. */
+size_t qeft_sz16_bytes(int oc, int m, int g);
+int qeft_pack_sz16(const float* scales, const float* zeros, int oc, int m, int g, void* sz16, void* stream);
 /* fp32 weak block [oc][k] (quantizer.py:52) -> weak16 [oc_pad][k_pad]. */
 int qeft_pack_weak(const float* weak, int oc, int k, int act_dtype, void* weak16, void* stream);
 /* QuantizedLinear.dequant_full (quantizer.py:95-100) of the device layer, fp32 [oc][ic]. */
@@ -109,8 +116,10 @@ int qeft_optq_codes(double* w64, const double* u64, const float* scales, const f
  * y[n][o] = sum_i W_hat[o][i] * x[n][i] for n < n_cols (1..16), x/y row-major.
  * y_f32 is a flags word: QEFT_Y_F32 (bit 0) writes fp32 y instead of act_dtype;
  * QEFT_Y_ACCUMULATE (bit 1) adds to y (y += W x, rounded once: a fused residual add).
- * Needs qeft_gemv_workspace_bytes() of scratch (the x gather buffer of irregular /
- * online-reorder layouts). */
+ * Needs qeft_gemv_workspace_bytes() of scratch: the split-K partials and per-row-block
+ * counters of the bulk-copy path (whose first bytes must be ZERO on entry; every call leaves
+ * them zero again -- do not share this scratch with other kernels), or the x gather buffer of
+ * the generic path. */
 size_t qeft_gemv_workspace_bytes(const qeft_linear_t* layer, int n_cols);
 int qeft_gemv(const qeft_linear_t* layer, const void* x, int64_t ldx, void* y, int64_t ldy, int y_f32,
               int n_cols, void* workspace, size_t workspace_bytes, void* stream);

@@ -27,7 +27,7 @@ class QeftLinearT(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "oc", "ic", "k", "bits", "g", "m", "ng", "m_pad", "k_pad", "oc_pad", "act_dtype", "flags")] + [
         ("qweight", ctypes.c_void_p), ("sz", ctypes.c_void_p), ("weak16", ctypes.c_void_p),
-        ("colmap", ctypes.c_void_p)]
+        ("colmap", ctypes.c_void_p), ("sz16", ctypes.c_void_p)]
 
 
 class ShadowDescT(ctypes.Structure):
@@ -43,6 +43,8 @@ SIGNATURES = {
     "qeft_repack_to_tiles": (_I, [_VP, _I, _I, _I, _VP, _VP]),
     "qeft_repack_to_ref": (_I, [_VP, _I, _I, _I, _VP, _VP]),
     "qeft_pack_sz": (_I, [_VP, _VP, _I, _I, _VP, _VP]),
+    "qeft_sz16_bytes": (_SZ, [_I, _I, _I]),
+    "qeft_pack_sz16": (_I, [_VP, _VP, _I, _I, _I, _VP, _VP]),
     "qeft_pack_weak": (_I, [_VP, _I, _I, _I, _VP, _VP]),
     "qeft_dequant_full": (_I, [_LP, _VP, _VP]),
     "qeft_gather_cols": (_I, [_VP, _I64, _VP, _I, _I, _I, _VP, _VP]),

@@ -57,6 +57,12 @@ int qeft_repack_to_ref(const void* qw, int oc, int m, int bits, uint8_t* ref, vo
   return repack_tiles_to_ref(qw, oc, m, bits, ref, ST(s));
 }
 
+size_t qeft_sz16_bytes(int oc, int m, int g) { return sz16_bytes(oc, m, g); }
+
+int qeft_pack_sz16(const float* sc, const float* zr, int oc, int m, int g, void* out, void* s) {
+  return pack_sz16(sc, zr, oc, m, g, out, ST(s));
+}
+
 int qeft_pack_sz(const float* sc, const float* zr, int oc, int ng, void* out, void* s) {
   return pack_sz(sc, zr, oc, ng, out, ST(s));
 }

@@ -657,9 +657,13 @@ int dispatch_gt(const GemvArgs& a, int gt, cudaStream_t st) {
 
 namespace qeft {
 
+// Workspace = [64 KB of row-block counters for the bulk-copy path (zero between calls)]
+//             [split-K partials (bulk-copy path) | x gather buffer (generic path)].
+constexpr size_t kWsHead = 64 * 1024;
+
 size_t gemv_workspace_bytes(const qeft_linear_t* L, int n) {
-  // gather buffer for layouts whose x cannot be read in place
-  return (size_t)n * (L->m_pad + L->k_pad) * 2 + 256;
+  const size_t gather = (size_t)n * (L->m_pad + L->k_pad) * 2 + 256;
+  return std::max(gemv2_workspace_bytes(L, n), kWsHead + gather);
 }
 
 int gemv_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ldx, void* const* ys, int64_t ldy,
@@ -668,6 +672,7 @@ int gemv_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ld
   const qeft_linear_t* L = Ls[0];
   QEFT_CHECK(n >= 1 && n <= 16, QEFT_ERR_SHAPE, "gemv: n_cols=%d outside 1..16", n);
   QEFT_CHECK(L->bits == 3 || L->bits == 4, QEFT_ERR_SHAPE, "gemv: bits=%d", L->bits);
+  bool v2 = true;
   GemvArgs a{};
   a.nl = nl;
   int rb_total = 0;
@@ -679,6 +684,7 @@ int gemv_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ld
                    (Li->colmap == L->colmap || (L->flags & QEFT_FLAG_STRUCTURED_FAST)),
                QEFT_ERR_SHAPE, "gemv: layer %d does not share the first layer's input geometry", l);
     QEFT_CHECK(ldx >= Li->ic && ldy >= Li->oc, QEFT_ERR_SHAPE, "gemv: ld too small");
+    v2 = v2 && gemv2_supported(Li, n);
     a.qw[l] = (const uint8_t*)Li->qweight;
     a.sz[l] = (const float2*)Li->sz;
     a.weak16[l] = (const uint8_t*)Li->weak16;
@@ -687,6 +693,15 @@ int gemv_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ld
     rb_total += Li->oc_pad / 16;
     a.rb_end[l] = rb_total;
   }
+  // bulk-copy warp-ring kernel (qeft_gemv2.cu) for group sizes that are multiples of 64;
+  // the per-element-dequant kernel below otherwise
+  if (v2) {
+    const int r = gemv2_multi(Ls, nl, x, ldx, ys, ldy, y_f32, n, ws, ws_bytes, st);
+    if (r != -1) return r;
+  }
+  QEFT_CHECK(ws_bytes >= kWsHead, QEFT_ERR_SHAPE, "gemv: workspace too small");
+  ws = (uint8_t*)ws + kWsHead;  // never touch the bulk-copy path's counters
+  ws_bytes -= kWsHead;
   a.ldy = ldy;
   a.y_f32 = y_f32;
   a.m = L->m; a.m_pad = L->m_pad; a.k = L->k; a.k_pad = L->k_pad;

@@ -34,6 +34,8 @@ inline int pad_to(int x, int a) { return (x + a - 1) / a * a; }
 int repack_ref_to_tiles(const uint8_t* ref, int oc, int m, int bits, void* qw, cudaStream_t st);
 int repack_tiles_to_ref(const void* qw, int oc, int m, int bits, uint8_t* ref, cudaStream_t st);
 int pack_sz(const float* s, const float* z, int oc, int ng, void* out, cudaStream_t st);
+size_t sz16_bytes(int oc, int m, int g);
+int pack_sz16(const float* s, const float* z, int oc, int m, int g, void* out, cudaStream_t st);
 int pack_weak(const float* w, int oc, int k, int dtype, void* out, cudaStream_t st);
 int dequant_full(const qeft_linear_t* L, float* out, cudaStream_t st);
 int gather_cols(const void* x, int64_t ldx, const int* colmap, int kk, int rows, int dtype, void* xb,
@@ -52,6 +54,12 @@ int gemv(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ld
          void* ws, size_t ws_bytes, cudaStream_t st);
 int gemv_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ldx, void* const* ys, int64_t ldy,
                int y_f32, int n, void* ws, size_t ws_bytes, cudaStream_t st);
+// bulk-copy warp-ring GEMV (qeft_gemv2.cu); gemv2_multi returns -1 when the launch needs the
+// generic path (its partials would not fit shared memory)
+bool gemv2_supported(const qeft_linear_t* L, int n);
+size_t gemv2_workspace_bytes(const qeft_linear_t* L, int n);
+int gemv2_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ldx, void* const* ys,
+                int64_t ldy, int y_f32, int n, void* ws, size_t ws_bytes, cudaStream_t st);
 
 size_t gemm_workspace_bytes(const qeft_linear_t* L, int T);
 int gemm_fwd(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ldy, int T,

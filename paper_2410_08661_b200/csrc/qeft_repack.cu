@@ -83,6 +83,20 @@ __global__ void pack_sz_kernel(const float* __restrict__ scales, const float* __
   sz[o + 1] = from_f32<T>(z);
 }
 
+// decode-GEMV copy of the group parameters: fp16 (scale, zero) half2 pairs laid out
+// [oc_pad/16][ng16][8][2] (ng16 = ceil(m_pad/g), zero beyond ng): the 16 rows of a (row-block,
+// group) are 64 contiguous bytes and rows r, r + 8 of the MMA fragment sit side by side.
+__global__ void pack_sz16_kernel(const float* __restrict__ scales, const float* __restrict__ zeros,
+                                 int oc, int oc_pad, int ng, int ng16, __half2* __restrict__ sz) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)oc_pad * ng16) return;
+  const int r = (int)(idx / ng16), gi = (int)(idx % ng16);
+  float s = 0.f, z = 0.f;
+  if (r < oc && gi < ng) { s = scales[(int64_t)r * ng + gi]; z = zeros[(int64_t)r * ng + gi]; }
+  const int rr = r & 15;
+  sz[(((int64_t)(r >> 4) * ng16 + gi) * 8 + (rr & 7)) * 2 + (rr >> 3)] = __floats2half2_rn(s, z);
+}
+
 template <typename T>
 __global__ void pack_weak_kernel(const float* __restrict__ weak, int oc, int k, int oc_pad,
                                  int k_pad, T* __restrict__ w16) {
@@ -154,6 +168,20 @@ int pack_sz(const float* s, const float* z, int oc, int ng, void* out, cudaStrea
   const int oc_pad = pad_to(oc, 16);
   if ((int64_t)oc_pad * ng == 0) return 0;
   pack_sz_kernel<float><<<nblk((int64_t)oc_pad * ng), 256, 0, st>>>(s, z, oc, oc_pad, ng, (float*)out);
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+size_t sz16_bytes(int oc, int m, int g) {
+  if (m <= 0 || g <= 0) return 0;
+  return (size_t)(pad_to(oc, 16) / 16) * ((pad_to(m, 128) + g - 1) / g) * 64;
+}
+
+int pack_sz16(const float* s, const float* z, int oc, int m, int g, void* out, cudaStream_t st) {
+  QEFT_CHECK(g > 0 && m >= 0, QEFT_ERR_SHAPE, "pack_sz16: g=%d m=%d", g, m);
+  if (m == 0) return 0;
+  const int oc_pad = pad_to(oc, 16), ng = (m + g - 1) / g, ng16 = (pad_to(m, 128) + g - 1) / g;
+  pack_sz16_kernel<<<nblk((int64_t)oc_pad * ng16), 256, 0, st>>>(s, z, oc, oc_pad, ng, ng16, (__half2*)out);
   QEFT_CUDA(cudaGetLastError());
   return 0;
 }

@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _lib
 from .errors import ShapeError
-from .layer import WORKSPACE, DeviceLayer, _pad, torch_dtype
+from .layer import GEMV_WORKSPACE, DeviceLayer, _pad, make_sz16, torch_dtype
 
 LLAMA_SHAPES = {
     # name -> (oc, ic) for one decoder block
@@ -59,7 +59,8 @@ def random_layer(oc, ic, k=128, bits=4, g=128, dtype="f16", seed=0, device="cuda
     colmap[m_pad:m_pad + k] = torch.arange(m, ic, dtype=torch.int32, device=device)
     return DeviceLayer(oc=oc, ic=ic, k=k, bits=bits, g=g, qweight=qweight, sz=sz.reshape(-1),
                        weak16=weak16, colmap=colmap, dtype=dtype,
-                       structured_fast=(m % 8 == 0 and ic % 8 == 0))
+                       structured_fast=(m % 8 == 0 and ic % 8 == 0),
+                       sz16=make_sz16(s[:oc].float(), z[:oc].float(), oc, m, g))
 
 
 def gemv_multi(layers, x, outs):
@@ -72,8 +73,8 @@ def gemv_multi(layers, x, outs):
     ldy = outs[0].stride(0) if n > 1 else max(l.oc for l in layers)
     if any((o.stride(0) if n > 1 else ldy) != ldy for o in outs):
         raise ShapeError("gemv_multi: outputs need a common row stride")
-    wsb = max(int(L.qeft_gemv_workspace_bytes(l.cptr, n)) for l in layers)
-    ws = WORKSPACE.get(wsb, x.device)
+    wsb = sum(int(L.qeft_gemv_workspace_bytes(l.cptr, n)) for l in layers)
+    ws = GEMV_WORKSPACE.get(wsb, x.device)
     ldx = x.stride(0) if n > 1 else layers[0].ic
     _lib.check(L.qeft_gemv_multi(ctypes.cast(arr, ctypes.c_void_p), len(layers), _lib.ptr(x), ldx,
                                  ctypes.cast(ys, ctypes.c_void_p), ldy,
@@ -114,8 +115,12 @@ class LinearStack:
         self.ics = sorted({l.ic for l in layers})
         # one input buffer per distinct input width, one output per layer
         self.x = {ic: torch.zeros((n_cols, ic), dtype=td, device=dev) for ic in self.ics}
-        self.y = [torch.empty((n_cols, l.oc), dtype=td, device=dev) for l in layers]
-        self.y_flat_host = torch.empty(sum(l.oc for l in layers) * n_cols, dtype=td).pin_memory()
+        # every layer's output is a column slice of ONE (n, sum oc) buffer: one D2H per step
+        tot = sum(l.oc for l in layers)
+        self.y_all = torch.empty((n_cols, tot), dtype=td, device=dev)
+        offs = np.concatenate([[0], np.cumsum([l.oc for l in layers])]).astype(int)
+        self.y = [self.y_all[:, offs[i]:offs[i + 1]] for i in range(len(layers))]
+        self.y_flat_host = torch.empty(tot * n_cols, dtype=td).pin_memory()
         self.x_host = {ic: torch.empty((n_cols, ic), dtype=td).pin_memory() for ic in self.ics}
         self.graph = None
         # warm the workspace and the kernels once eagerly
@@ -166,11 +171,7 @@ class LinearStack:
         for ic in self.ics:
             self.x[ic].copy_(self.x_host[ic], non_blocking=True)
         self.step()
-        off = 0
-        for y in self.y:
-            n = y.numel()
-            self.y_flat_host[off:off + n].copy_(y.reshape(-1), non_blocking=True)
-            off += n
+        self.y_flat_host.copy_(self.y_all.reshape(-1), non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return self.y_flat_host
 

@@ -97,7 +97,8 @@ def _with_perm(q, dl, perm):
     colmap[:q.m] = p[:q.m]
     colmap[dl.m_pad:dl.m_pad + q.k] = p[q.m:]
     return DeviceLayer(oc=q.oc, ic=q.ic, k=q.k, bits=q.bits, g=q.g, qweight=dl.qweight, sz=dl.sz,
-                       weak16=dl.weak16, colmap=torch.from_numpy(colmap).cuda(), dtype=dl.dtype)
+                       weak16=dl.weak16, colmap=torch.from_numpy(colmap).cuda(), dtype=dl.dtype,
+                       sz16=dl.sz16)
 
 
 def matvec_structured(q, x, stats: KernelStats | None = None) -> np.ndarray:

@@ -3,7 +3,10 @@ calls into the CUDA library (GEMV / GEMM / dequant).
 
 HBM layout of one layer (all on one GPU; see csrc/qeft_common.cuh):
   qweight  uint8   (oc_pad/16) row-blocks x K-tiles of 512 B (4-bit) / 768 B (3-bit)
-  sz       fp32    (scale, zero) pairs [oc_pad/16][ng][16][2] (the reference's storage precision)
+  sz       fp32    (scale, zero) pairs [oc_pad/16][ng][16][2] (the reference's storage precision;
+                   read by the GEMMs, the dequant and the generic-g GEMV)
+  sz16     fp16    decode-GEMV copy of (scale, zero): half2 [oc_pad/16][ng16][8][2], 4 B per row
+                   and group, ng16 = ceil(m_pad/g)
   weak16   dtype   [oc_pad][k_pad]  (the trainable block's kernel shadow)
   colmap   int32   [m_pad + k_pad]  B200 K position -> input column (-1 padding)
   weak32   fp32    [oc][k]          trainable master (a view into the DP bucket
@@ -49,13 +52,27 @@ class _Workspace:
 
 
 WORKSPACE = _Workspace()
+# the decode GEMV's scratch: its head holds split-K row-block counters that must stay zero
+# between calls, so it is never shared with the GEMMs' gather buffers
+GEMV_WORKSPACE = _Workspace()
+
+
+def make_sz16(scales, zeros, oc: int, m: int, g: int):
+    """fp32 scales/zeros CUDA tensors [oc][ng] -> the GEMV's fp16 (scale, zero) copy."""
+    import torch
+    L = _lib.lib()
+    out = torch.zeros(max(int(L.qeft_sz16_bytes(oc, m, g)), 16), dtype=torch.uint8, device=scales.device)
+    if m > 0:
+        _lib.check(L.qeft_pack_sz16(_lib.ptr(scales.contiguous()), _lib.ptr(zeros.contiguous()), oc, m, g,
+                                    _lib.ptr(out), _lib.stream_ptr()), "pack_sz16")
+    return out
 
 
 class DeviceLayer:
     """A QuantizedLinear converted to the B200 layout on the current GPU."""
 
     def __init__(self, *, oc, ic, k, bits, g, qweight, sz, weak16, colmap, dtype="f16",
-                 weak32=None, structured_fast=False, source_id=None):
+                 weak32=None, structured_fast=False, source_id=None, sz16=None):
         import torch
         self.oc, self.ic, self.k, self.bits, self.g = oc, ic, k, bits, g
         self.m = ic - k
@@ -64,6 +81,7 @@ class DeviceLayer:
         self.dtype = dtype
         self.tdtype = torch_dtype(dtype)
         self.qweight, self.sz, self.weak16, self.colmap = qweight, sz, weak16, colmap
+        self.sz16 = sz16
         self.weak32 = weak32
         self.structured_fast = structured_fast
         self.source_id = source_id
@@ -79,6 +97,7 @@ class DeviceLayer:
         s.sz = self.sz.data_ptr()
         s.weak16 = self.weak16.data_ptr() if self.weak16 is not None and self.weak16.numel() else None
         s.colmap = self.colmap.data_ptr()
+        s.sz16 = self.sz16.data_ptr() if self.sz16 is not None else None
         self.cstruct = s
         self.cptr = ctypes.pointer(s)
 
@@ -128,7 +147,8 @@ class DeviceLayer:
                        "pack_weak")
         return cls(oc=oc, ic=ic, k=k, bits=bits, g=g, qweight=qweight, sz=sz, weak16=weak16,
                    colmap=torch.from_numpy(colmap).to(device), dtype=dtype,
-                   weak32=weak32.reshape(oc, k), structured_fast=fast, source_id=_source_id(q))
+                   weak32=weak32.reshape(oc, k), structured_fast=fast, source_id=_source_id(q),
+                   sz16=make_sz16(sc, zr, oc, m, g))
 
     # ------------------------------------------------------------------
     def refresh_weak16(self):
@@ -172,9 +192,11 @@ class DeviceLayer:
                               device=x.device)
         L = _lib.lib()
         wsb = int(L.qeft_gemv_workspace_bytes(self.cptr, n))
-        ws = WORKSPACE.get(wsb, x.device)
+        ws = GEMV_WORKSPACE.get(wsb, x.device)
         ldx = x.stride(0) if n > 1 else self.ic      # size-1 dims may carry any stride
         ldy = out.stride(0) if n > 1 else self.oc
+        if out.stride(1) != 1 or (n > 1 and ldy < self.oc):
+            raise ShapeError("gemv: out must be row-major with unit column stride")
         flags = (1 if out.dtype == torch.float32 else 0) | (2 if accumulate else 0)
         _lib.check(L.qeft_gemv(self.cptr, _lib.ptr(x), ldx, _lib.ptr(out), ldy, flags, n, _lib.ptr(ws),
                                ws.numel(), _lib.stream_ptr()), "gemv")

@@ -34,7 +34,7 @@ def test_library_exports_every_header_symbol():
 
 def test_struct_layout():
     from paper_2410_08661_b200 import _lib
-    assert ctypes.sizeof(_lib.QeftLinearT) == 12 * 4 + 4 * 8
+    assert ctypes.sizeof(_lib.QeftLinearT) == 12 * 4 + 5 * 8
     assert _lib.QeftLinearT.qweight.offset == 48
     assert ctypes.sizeof(_lib.ShadowDescT) == 32
 
