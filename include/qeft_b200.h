@@ -124,6 +124,12 @@ size_t qeft_gemv_workspace_bytes(const qeft_linear_t* layer, int n_cols);
 int qeft_gemv(const qeft_linear_t* layer, const void* x, int64_t ldx, void* y, int64_t ldy, int y_f32,
               int n_cols, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Profiling only: slots > 0 arms per-CTA globaltimer stamps for the next `slots` bulk-copy
+ * GEMV launches (8 x u64 per CTA, 512 CTAs per slot: start, after the PDL wait, after x
+ * staging, first stage landed (warp 0), loop done (warp 0), all warps done, end); slots == 0
+ * copies them to host_out (slots x 512 x 8 u64, may be NULL) and disarms. */
+int qeft_gemv_trace(int slots, unsigned long long* host_out);
+
 /* Several layers that read the same x in ONE launch (a decoder's q/k/v or gate/up): their
  * rows are concatenated, each layer writes its own y (ys[l], common ldy). Up to 3 layers with
  * identical ic, k, bits, g, act_dtype, flags (and column map). */

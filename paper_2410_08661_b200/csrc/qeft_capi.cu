@@ -101,6 +101,8 @@ int qeft_quantize_rtn(const float* w, int oc, int m, int g, int bits, float* sc,
   return quantize_rtn(w, oc, m, g, bits, sc, zr, codes, ST(s));
 }
 
+int qeft_gemv_trace(int slots, unsigned long long* host_out) { return gemv_trace(slots, host_out); }
+
 size_t qeft_gemv_workspace_bytes(const qeft_linear_t* L, int n) { return gemv_workspace_bytes(L, n); }
 
 int qeft_gemv(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ldy, int y_f32,

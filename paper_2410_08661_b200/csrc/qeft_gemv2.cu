@@ -6,21 +6,22 @@
 //
 // Why this shape (measured on B200, scripts/micro/bulk_warp_bench.cu, profiles/r02):
 //   * every warp owns a private ring of R stages fed by its OWN lane 0 with 1-D bulk copies
-//     (cp.async.bulk, the TMA engine) completing on an mbarrier: 8 warps x 3 x 4 KB per SM
-//     streams 6.9-7.0 TB/s. No per-lane address arithmetic, no producer/consumer handshake
+//     (cp.async.bulk, the TMA engine) completing on an mbarrier: 8-16 warps x 2-3 x 4 KB per
+//     SM stream 6.9-7.0 TB/s. No per-lane address arithmetic, no producer/consumer handshake
 //     across warps: a warp waits on its own barrier, decodes, multiplies, and refills.
 //   * work split: a thread-block cluster of S CTAs owns a contiguous run of row-blocks (16
 //     output rows each); CTA rank r streams K slice r of every one of them (slices are whole
-//     groups, balanced by bytes). Inside a CTA the run's stages (4 KB each) are dealt to the
-//     8 warps round-robin, so every warp streams the same number of bytes. Partials go to
-//     shared memory; at the end the 8 warp partials and then the S slice partials (over
-//     DSMEM) are summed in a fixed order: deterministic, no atomics, no global scratch.
+//     groups, balanced by bytes; S = 1 unless the row-blocks do not spread evenly over the
+//     SMs). Inside a CTA the run's stages (4 KB each) are dealt to the warps round-robin.
+//     Partials go to shared memory; at the end the warp partials and then the S slice
+//     partials (over DSMEM) are summed in a fixed order: deterministic, no atomics, no
+//     global scratch.
 //   * x is staged once per CTA for its K slice only (gathered through the column map for
 //     irregular / online layouts, so no separate gather launch), with the per-(group,
 //     column) sums of x that the zero-point fold needs.
 //   * codes become (magic + code) half2 A fragments with one LOP3 each (qeft_common.cuh
 //     decode4 / decode3_pair) for mma.sync m16n8k16 (x is the B operand: 8 columns per MMA
-//     at no extra cost), and every group is folded as
+//     at no extra cost); one MMA chain per group, then the group is folded as
 //       acc += s' * sum(c' x) + (z - magic * s') * sum(x)     (fp32)
 //     with (scale, zero) read as an fp16 pair (sz16, 4 B per row and group: SURVEY 7.3).
 //   * programmatic dependent launch: each warp issues its first weight stages BEFORE
@@ -37,16 +38,20 @@ using namespace qeft;
 
 namespace {
 
-// Launch shape (template): NW warps per CTA, CPS 128-column chunks per codes stage (a stage
-// holds CPS * 1 KB of 4-bit codes + their sz16 pairs, or CPS / 2 weak tiles), R stages per ring.
-constexpr int kMaxS = 4;            // K slices = cluster size
-constexpr int kMaxL = 3;            // layers per launch
-constexpr int kMaxJ = 48;           // row-blocks per cluster (partials live in shared memory)
+constexpr int kMaxS = 4;   // K slices = cluster size
+constexpr int kMaxL = 3;   // layers per launch
+constexpr int kMaxJ = 48;  // row-blocks per cluster (partials live in shared memory)
 
 int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
   return v ? atoi(v) : dflt;
 }
+
+// one K slice, precomputed on the host: codes chunks [c0, c1), weak tiles [w0, w1), staged
+// B200 columns [kb, ke), x-sum groups [gx0, gx0 + ngx), codes / total stages per row-block
+struct SliceGeo {
+  int c0, c1, w0, w1, kb, ke, gx0, ngx, ncs, nst;
+};
 
 struct G2Args {
   const uint8_t* qw[kMaxL];
@@ -64,33 +69,19 @@ struct G2Args {
   int yflags;  // QEFT_Y_F32 | QEFT_Y_ACCUMULATE
   int m, m_pad, k, k_pad, g, n, n_rb;
   int nch;   // m_pad / 128 chunks
-  int U;     // chunks per slicing unit (whole groups)
-  int nuc;   // codes units
   int ng16;  // sz16 groups per row-block
   int S;     // K slices (cluster size)
-  int ub[kMaxS + 1];
+  SliceGeo geo[kMaxS];
   int J;        // row-blocks per cluster
   int xs_ld;    // staged x row stride (elements)
   int64_t rbb;  // qweight bytes per row-block
+  unsigned long long* trace;  // profiling only (qeft_gemv_trace): per-CTA timestamps, or null
 };
 
-struct Slice {
-  int c0, c1, w0, w1;
-};
-
-QEFT_DEV Slice slice_of(const G2Args& a, int s) {
-  const int u0 = a.ub[s], u1 = a.ub[s + 1];
-  Slice r;
-  r.c0 = min(min(u0, a.nuc) * a.U, a.nch);
-  r.c1 = min(min(u1, a.nuc) * a.U, a.nch);
-  r.w0 = max(u0, a.nuc) - a.nuc;
-  r.w1 = max(u1, a.nuc) - a.nuc;
-  return r;
-}
-
-// B200 K position where unit boundary u starts
-QEFT_DEV int kpos(const G2Args& a, int u) {
-  return u <= a.nuc ? min(u * a.U, a.nch) * 128 : a.m_pad + (u - a.nuc) * 64;
+QEFT_DEV unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
 QEFT_DEV int layer_of(const G2Args& a, int j, int& lrb) {
@@ -103,39 +94,46 @@ QEFT_DEV int layer_of(const G2Args& a, int j, int& lrb) {
 QEFT_DEV uint4 lds128(const void* p) { return *reinterpret_cast<const uint4*>(p); }
 QEFT_DEV uint2 lds64(const void* p) { return *reinterpret_cast<const uint2*>(p); }
 
-template <int BITS, int NT, int GT, typename T, int R, int NW, int CPS>
-__global__ void __launch_bounds__(NW * 32, 1) gemv2_kernel(const G2Args a) {
-  constexpr int kNW = NW, kCPS = CPS, kWPS = CPS / 2;
+// Launch shape (template): NW warps per CTA, CPS 128-column chunks per codes stage (a stage
+// holds CPS KB of 4-bit codes + their sz16 pairs, or CPS / 2 weak tiles), R stages per ring.
+// ONE: a single activation column (batch-1 decode): only column 0 of the MMA output is live.
+template <int BITS, int NT, int GT, typename T, int R, int NW, int CPS, bool ONE, int MINB, int PRE>
+__global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
+  constexpr int kWPS = CPS / 2;
   constexpr int kSzOff = CPS * 1024, kStage = CPS * 1152;  // codes, then sz16 pairs
-  constexpr int NTS = NT * 8;                 // x-sum column stride
-  constexpr int CB = BITS == 4 ? 1024 : 768;  // bytes per 128-column chunk of 16 rows
-  constexpr int HG = GT >= 2 ? GT / 2 : 1;    // chunks per group (GT >= 2)
+  constexpr int NTS = NT * 8;                               // x-sum column stride
+  constexpr int CB = BITS == 4 ? 1024 : 768;                // bytes per 128-column chunk
+  constexpr int HG = GT >= 2 ? GT / 2 : 1;                  // chunks per group (GT >= 2)
+  static_assert(GT <= 2 * CPS && (2 * CPS) % GT == 0, "a full stage must hold whole groups");
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[kNW][R];
+  __shared__ __align__(8) uint64_t full[NW][R];
+  __shared__ __align__(8) uint64_t xbar;  // x staging (bulk copies)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g8 = lane >> 2, t4 = lane & 3;
   const int rank = a.S > 1 ? (int)cluster_ctarank() : 0;
-  const int clu = blockIdx.x / a.S;
+  const int clu = a.S > 1 ? blockIdx.x / a.S : blockIdx.x;
+  const int n = ONE ? 1 : a.n;
+  unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * 8 : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = gtime();
 
-  // shared memory: [rings][partials red: J x kNW x 16 x n floats][x: n x xs_ld][x sums]
+  // shared memory: [rings][partials red: J x NW x 16 x n floats][x: n x xs_ld][x sums]
   uint8_t* ring = smem + (size_t)warp * R * kStage;
-  float* red = reinterpret_cast<float*>(smem + (size_t)kNW * R * kStage);
-  const int redn = 16 * a.n;  // floats per (row-block, warp)
-  T* xs = reinterpret_cast<T*>(red + (size_t)a.J * kNW * redn);
-  float* xsum = reinterpret_cast<float*>(xs + (size_t)a.n * a.xs_ld);
+  float* red = reinterpret_cast<float*>(smem + (size_t)NW * R * kStage);
+  const int redn = 16 * n;  // floats per (row-block, warp)
+  T* xs = reinterpret_cast<T*>(red + (size_t)a.J * NW * redn);
+  float* xsum = reinterpret_cast<float*>(xs + (size_t)n * a.xs_ld);
 
-  // this CTA: row-blocks [j0, j1) of the cluster, K slice `rank`; stages of row-block jl are
-  // jl * nst .. jl * nst + nst - 1 (codes stages, then weak stages); warp w takes w, w + 8, ...
-  const int j0 = clu * a.J, j1 = min(j0 + a.J, a.n_rb), nj = max(j1 - j0, 0);
-  const Slice sl = slice_of(a, rank);
-  const int ncs = (sl.c1 - sl.c0 + kCPS - 1) / kCPS;
-  const int nst = ncs + (sl.w1 - sl.w0 + kWPS - 1) / kWPS;
+  // this CTA: row-blocks [j0, j0 + nj) of the cluster, K slice `rank`; stages of row-block jl
+  // are jl * nst .. jl * nst + nst - 1 (codes stages, then weak stages); warp w takes w, w + NW..
+  const SliceGeo sg = a.geo[rank];
+  const int j0 = clu * a.J, nj = max(min(a.J, a.n_rb - j0), 0);
+  const int ncs = sg.ncs, nst = sg.nst;
   const int total = nj * nst;
-  const int my_n = warp < total ? (total - warp + kNW - 1) / kNW : 0;
+  const int my_n = warp < total ? (total - warp + NW - 1) / NW : 0;
 
-  // ---- lane 0: bulk-copy issue (stage i of this warp = global stage warp + i * kNW) ----
+  // ---- lane 0: bulk-copy issue (stage i of this warp = global stage warp + i * NW) ----
   int issued = 0;
-  int is_jl = warp / max(nst, 1), is_t = warp - is_jl * nst;
+  int is_jl = warp / nst, is_t = warp - is_jl * nst;
   const uint8_t *pq = nullptr, *ps = nullptr, *pw = nullptr;  // row-block is_jl's streams
   auto rb_ptrs = [&]() {
     int lrb;
@@ -152,7 +150,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv2_kernel(const G2Args a) {
     uint8_t* dst = ring + slot * kStage;
     uint64_t* bar = &full[warp][slot];
     if (is_t < ncs) {
-      const int ca = sl.c0 + is_t * kCPS, cb = min(ca + kCPS, sl.c1);
+      const int ca = sg.c0 + is_t * CPS, cb = min(ca + CPS, sg.c1);
       const int ga = GT == 1 ? 2 * ca : ca / HG;
       const int gb = GT == 1 ? 2 * cb : (cb + HG - 1) / HG;
       const uint32_t cbytes = (uint32_t)(cb - ca) * CB, sbytes = (uint32_t)(gb - ga) * 64;
@@ -160,13 +158,13 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv2_kernel(const G2Args a) {
       bulk_g2s(dst, pq + ca * CB, cbytes, bar);
       bulk_g2s(dst + kSzOff, ps + ga * 64, sbytes, bar);
     } else {
-      const int wa = sl.w0 + (is_t - ncs) * kWPS, wb = min(wa + kWPS, sl.w1);
+      const int wa = sg.w0 + (is_t - ncs) * kWPS, wb = min(wa + kWPS, sg.w1);
       const uint32_t bytes = (uint32_t)(wb - wa) * 2048;
       mbar_expect_tx(bar, bytes);
       bulk_g2s(dst, pw + wa * 2048, bytes, bar);
     }
     ++issued;
-    is_t += kNW;
+    is_t += NW;
     if (is_t >= nst) {
       do {
         is_t -= nst;
@@ -179,63 +177,109 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv2_kernel(const G2Args a) {
 
   if (lane == 0) {
     for (int i = 0; i < R; ++i) mbar_init(&full[warp][i], 1);
+    if (warp == 0) mbar_init(&xbar, 1);
     fence_mbar_init();
   }
   __syncwarp();
-  // weight stages (codes + group params: never written by a preceding kernel) go out first
-  if (lane == 0)
-    while (issued < R && issue(true)) {
-    }
+  // PRE > 0: weight stages (codes + group params, never written by a preceding kernel) go out
+  // before the PDL wait -- worth it only when this CTA can start beside the previous kernel's
   pdl_launch_dependents();
+  if constexpr (PRE > 0) {
+    if (lane == 0)
+      while (issued < PRE && issue(true)) {
+      }
+  }
+  if (tr && threadIdx.x == 0) tr[7] = gtime();
   pdl_wait();
+  __syncthreads();  // xbar initialised before thread 0 arms it
+  if (tr && threadIdx.x == 0) tr[1] = gtime();
 
   // ---- stage x (B200 K order) for this CTA's K slice; zero the partials ----
-  const int kb = kpos(a, a.ub[rank]), ke = kpos(a, a.ub[rank + 1]);
-  const int ncols = ke - kb;
-  for (int e = threadIdx.x; e < nj * kNW * redn; e += kNW * 32) red[e] = 0.f;
+  const int kb = sg.kb, ncols = sg.ke - sg.kb;
+  for (int e = threadIdx.x; e < nj * NW * redn; e += NW * 32) red[e] = 0.f;
   {
     const T zero = from_f32<T>(0.f);
     const T* x = reinterpret_cast<const T*>(a.x);
     if (a.fast) {
-      const int n8 = ncols >> 3;
-      for (int e = threadIdx.x; e < a.n * n8; e += kNW * 32) {
-        const int n = e / n8, c = (e - n * n8) << 3, kk = kb + c;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        int col = -1;
-        if (kk < a.m_pad) {
-          if (kk < a.m) col = kk;
-        } else if (kk - a.m_pad < a.k) {
-          col = a.m + kk - a.m_pad;
+      // structured layout: the slice's x is (at most) two contiguous runs per row -- quantized
+      // columns [kb, min(ke, m)) and weak columns -- moved by bulk copies; padding zeroed here
+      const int q1 = min(sg.ke, a.m);
+      const int w_beg = max(kb, a.m_pad), w_end = min(sg.ke, a.m_pad + a.k);
+      if (threadIdx.x == 0) {
+        const uint32_t bytes =
+            (uint32_t)n * 2u * (uint32_t)(max(q1 - kb, 0) + max(w_end - w_beg, 0));
+        if (bytes) {
+          mbar_expect_tx(&xbar, bytes);
+          for (int r = 0; r < n; ++r) {
+            if (q1 > kb) bulk_g2s(xs + r * a.xs_ld, x + r * a.ldx + kb, (uint32_t)(q1 - kb) * 2u, &xbar);
+            if (w_end > w_beg)
+              bulk_g2s(xs + r * a.xs_ld + (w_beg - kb), x + r * a.ldx + a.m + (w_beg - a.m_pad),
+                       (uint32_t)(w_end - w_beg) * 2u, &xbar);
+          }
+        } else {
+          mbar_arrive(&xbar);
         }
-        if (col >= 0) v = *reinterpret_cast<const uint4*>(x + n * a.ldx + col);
-        *reinterpret_cast<uint4*>(xs + n * a.xs_ld + c) = v;
       }
+      __syncthreads();  // x goes into the copy queue ahead of the weight stream
+      if (lane == 0)
+        while (issued < R && issue(false)) {
+        }
+      // zero padding: quantized [m, m_pad) and weak [m_pad + k, m_pad + k_pad) inside the slice
+      const int z0a = max(kb, a.m), z0b = min(sg.ke, a.m_pad);
+      const int z1a = max(kb, a.m_pad + a.k), z1b = sg.ke;
+      const int nz0 = max(z0b - z0a, 0), nz1 = max(z1b - z1a, 0);
+      for (int e = threadIdx.x; e < n * (nz0 + nz1); e += NW * 32) {
+        const int r = ONE ? 0 : e / (nz0 + nz1), c = e - r * (nz0 + nz1);
+        xs[r * a.xs_ld + (c < nz0 ? z0a + c : z1a + c - nz0) - kb] = zero;
+      }
+      mbar_wait(&xbar, 0);
     } else {
-      for (int e = threadIdx.x; e < a.n * ncols; e += kNW * 32) {
-        const int n = e / ncols, c = e - n * ncols;
-        const int col = a.colmap[kb + c];
-        xs[n * a.xs_ld + c] = col >= 0 ? x[n * a.ldx + col] : zero;
+      if (lane == 0)
+        while (issued < R && issue(false)) {
+        }
+      // column map (irregular / online layouts): gather, 4 loads in flight per thread
+      const int tot = n * ncols;
+      for (int e0 = threadIdx.x; e0 < tot; e0 += 4 * NW * 32) {
+        int col[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = e0 + u * NW * 32;
+          const int r = ONE ? 0 : e / ncols, c = e - r * ncols;
+          col[u] = e < tot ? a.colmap[kb + c] : -1;
+        }
+        T v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = e0 + u * NW * 32;
+          const int r = ONE ? 0 : e / ncols;
+          v[u] = col[u] >= 0 ? x[r * a.ldx + col[u]] : zero;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = e0 + u * NW * 32;
+          const int r = ONE ? 0 : e / ncols, c = e - r * ncols;
+          if (e < tot) xs[r * a.xs_ld + c] = v[u];
+        }
       }
     }
   }
   __syncthreads();
   // per-(group, column) sums of x over the staged quantized columns: 16 lanes per pair,
   // fixed-order tree reduction (deterministic)
-  const int gx0 = kb < a.m_pad ? kb / a.g : 0;
-  const int qend = min(ke, a.m_pad);
-  const int ngx = kb < a.m_pad ? (qend - gx0 * a.g + a.g - 1) / a.g : 0;
+  const int gx0 = sg.gx0, ngx = sg.ngx;
   {
     using T2 = typename DTraits<T>::T2;
     const int half = lane >> 4, l16 = lane & 15;
+    const int qend = min(sg.ke, a.m_pad);
     // warp-uniform trip count (the shuffles need all 32 lanes); an odd tail half idles
-    for (int p0 = warp * 2; p0 < ngx * a.n; p0 += kNW * 2) {
+    for (int p0 = warp * 2; p0 < ngx * n; p0 += NW * 2) {
       const int p = p0 + half;
-      const bool live = p < ngx * a.n;
-      const int gi = live ? p / a.n : 0, n = live ? p - gi * a.n : 0;
+      const bool live = p < ngx * n;
+      const int gi = !live ? 0 : ONE ? p : p / n, r = live && !ONE ? p - gi * n : 0;
       const int c_beg = (gx0 + gi) * a.g, c_end = live ? min(c_beg + a.g, qend) : c_beg;
       float sum = 0.f;
       for (int c = c_beg + l16 * 8; c < c_end; c += 128) {
-        const uint4 v = lds128(xs + n * a.xs_ld + (c - kb));
+        const uint4 v = lds128(xs + r * a.xs_ld + (c - kb));
         const T2* h = reinterpret_cast<const T2*>(&v);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -245,21 +289,20 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv2_kernel(const G2Args a) {
       }
 #pragma unroll
       for (int o = 8; o >= 1; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      if (l16 == 0 && live) xsum[gi * NTS + n] = sum;
+      if (l16 == 0 && live) xsum[gi * NTS + r] = sum;
     }
   }
   __syncthreads();
+  if (tr && threadIdx.x == 0) tr[2] = gtime();
 
   // ---- consume ----
   if (lane == 0)
     while (issued < R && issue(false)) {
     }
-  int xrow[NT];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) xrow[nt] = min(g8 + 8 * nt, a.n - 1);
   const T* xlane[NT];  // this lane's staged x row, at its 16-column offset inside a step
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt) xlane[nt] = xs + xrow[nt] * a.xs_ld + 16 * t4 - kb;
+  for (int nt = 0; nt < NT; ++nt) xlane[nt] = xs + min(g8 + 8 * nt, n - 1) * a.xs_ld + 16 * t4 - kb;
+  const float* xsl = xsum + 2 * t4 - gx0 * NTS;  // this lane's x-sum columns, by group
   float acc[NT][4];
   auto zero4 = [](float (&v)[NT][4]) {
 #pragma unroll
@@ -308,8 +351,8 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv2_kernel(const G2Args a) {
         for (int pp = 0; pp < 4; ++pp) f[jj][pp] = decode3_pair<T>(ww2[jj >> 1], hbits, 4 * (jj & 1) + pp, jj >> 1);
     }
   };
-  // acc += s' * sum(c' x) + (z - magic s') * sum(x) for one group (sz16 pair at szp)
-  auto fold = [&](const uint8_t* szp, int gx, const float (&gsum)[NT][4]) {
+  // acc += s' * sum(c' x) + (z - magic s') * sum(x) for group grp (sz16 pair at szp)
+  auto fold = [&](const uint8_t* szp, int grp, const float (&gsum)[NT][4]) {
     constexpr float M = DTraits<T>::kMagicF;
     const uint2 p = lds64(szp + g8 * 8);
     const float2 r0 = __half22float2(*reinterpret_cast<const __half2*>(&p.x));
@@ -317,30 +360,57 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv2_kernel(const G2Args a) {
     const float s0 = r0.x;
     const float s1 = (BITS == 4 && DTraits<T>::kHiTrick) ? r1.x * (1.f / 16.f) : r1.x;
     const float z0 = fmaf(-M, s0, r0.y), z1 = fmaf(-M, s1, r1.y);
+    if constexpr (ONE) {  // column 0 only (lanes t4 == 0 carry it; the others are discarded)
+      const float sx = xsl[grp * NTS];
+      acc[0][0] = fmaf(s0, gsum[0][0], fmaf(z0, sx, acc[0][0]));
+      acc[0][2] = fmaf(s1, gsum[0][2], fmaf(z1, sx, acc[0][2]));
+    } else {
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const float2 sx = *reinterpret_cast<const float2*>(xsum + gx * NTS + 8 * nt + 2 * t4);
-      acc[nt][0] = fmaf(s0, gsum[nt][0], fmaf(z0, sx.x, acc[nt][0]));
-      acc[nt][1] = fmaf(s0, gsum[nt][1], fmaf(z0, sx.y, acc[nt][1]));
-      acc[nt][2] = fmaf(s1, gsum[nt][2], fmaf(z1, sx.x, acc[nt][2]));
-      acc[nt][3] = fmaf(s1, gsum[nt][3], fmaf(z1, sx.y, acc[nt][3]));
+      for (int nt = 0; nt < NT; ++nt) {
+        const float2 sx = *reinterpret_cast<const float2*>(xsl + grp * NTS + 8 * nt);
+        acc[nt][0] = fmaf(s0, gsum[nt][0], fmaf(z0, sx.x, acc[nt][0]));
+        acc[nt][1] = fmaf(s0, gsum[nt][1], fmaf(z0, sx.y, acc[nt][1]));
+        acc[nt][2] = fmaf(s1, gsum[nt][2], fmaf(z1, sx.x, acc[nt][2]));
+        acc[nt][3] = fmaf(s1, gsum[nt][3], fmaf(z1, sx.y, acc[nt][3]));
+      }
     }
   };
+  // NCK whole chunks starting at chunk ca, straight-line: one MMA chain per group, then folds
+  auto codes_stage = [&](auto nck_c, const uint8_t* st, int ca) {
+    constexpr int NCK = decltype(nck_c)::value;
+    constexpr int NG = 2 * NCK / GT;
+    const int ga = GT == 1 ? 2 * ca : ca / HG;
+    float d[NG][NT][4];
+#pragma unroll
+    for (int q = 0; q < NG; ++q) zero4(d[q]);
+#pragma unroll
+    for (int s = 0; s < 2 * NCK; ++s) {
+      uint32_t f[4][4];
+      decode_step(st + (s >> 1) * CB, s & 1, f);
+      mma_step(f, ca * 128 + s * 64, d[s / GT]);
+    }
+#pragma unroll
+    for (int q = 0; q < NG; ++q) fold(st + kSzOff + q * 64, ga + q, d[q]);
+  };
   auto park = [&](int jl) {  // this warp's partial of row-block jl -> shared memory
-    float* rp = red + ((size_t)jl * kNW + warp) * redn;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int row = g8 + 8 * (e >> 1), col = 8 * nt + 2 * t4 + (e & 1);
-        if (col < a.n) rp[row * a.n + col] = acc[nt][e];
+    float* rp = red + ((size_t)jl * NW + warp) * redn;
+    if constexpr (ONE) {
+      if (t4 == 0) {
+        rp[g8] = acc[0][0];
+        rp[g8 + 8] = acc[0][2];
       }
+    } else {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int row = g8 + 8 * (e >> 1), col = 8 * nt + 2 * t4 + (e & 1);
+          if (col < n) rp[row * n + col] = acc[nt][e];
+        }
+    }
   };
 
-  // steps per group (64-column steps): full codes stages hold 8 steps = 8 / GT groups
-  constexpr int kSteps = 2 * kCPS;
-  constexpr int kGPS = GT <= kSteps ? kSteps / GT : 1;
-  int jl = warp / max(nst, 1), t = warp - jl * nst;  // stage (row-block, index) under this warp
+  int jl = warp / nst, t = warp - jl * nst;  // stage (row-block, index) under this warp
   int cur_jl = jl;
   int slot = 0;
   uint32_t phase = 0;
@@ -351,45 +421,42 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv2_kernel(const G2Args a) {
       cur_jl = jl;
     }
     mbar_wait(&full[warp][slot], phase);
+    if (tr && threadIdx.x == 0 && i == 0) tr[3] = gtime();
     const uint8_t* st = ring + slot * kStage;
     if (t < ncs) {
-      const int ca = sl.c0 + t * kCPS, nck = min(kCPS, sl.c1 - ca);
-      const int ga = GT == 1 ? 2 * ca : ca / HG;
-      const int kc = ca * 128;  // B200 column of the stage's first code
-      if (nck == kCPS && (GT <= kSteps)) {
-        // full stage: 8 steps, one MMA chain per group, folded after the chain
-        float d[kGPS][NT][4];
-#pragma unroll
-        for (int q = 0; q < kGPS; ++q) zero4(d[q]);
-#pragma unroll
-        for (int sidx = 0; sidx < kSteps; ++sidx) {
-          uint32_t f[4][4];
-          decode_step(st + (sidx >> 1) * CB, sidx & 1, f);
-          mma_step(f, kc + sidx * 64, d[sidx / (GT <= kSteps ? GT : 1)]);
-        }
-#pragma unroll
-        for (int q = 0; q < kGPS; ++q) {
-          const int grp = (GT == 1 ? 2 * ca : ca / HG) + q;
-          fold(st + kSzOff + (grp - ga) * 64, grp - gx0, d[q]);
+      const int ca = sg.c0 + t * CPS, nck = min(CPS, sg.c1 - ca);
+      if (nck == CPS) {
+        codes_stage(std::integral_constant<int, CPS>{}, st, ca);
+      } else if (GT <= 2 || (nck % HG) == 0) {
+        // end of a slice (whole groups): straight-line code per chunk count
+        switch (nck) {
+          case 1: if constexpr (GT <= 2) codes_stage(std::integral_constant<int, 1>{}, st, ca); break;
+          case 2: if constexpr (GT <= 4 && 2 < CPS) codes_stage(std::integral_constant<int, 2>{}, st, ca); break;
+          case 3: if constexpr (GT <= 2 && 3 < CPS) codes_stage(std::integral_constant<int, 3>{}, st, ca); break;
+          case 4: if constexpr (4 < CPS) codes_stage(std::integral_constant<int, (4 < CPS ? 4 : 1)>{}, st, ca); break;
+          case 5: if constexpr (GT <= 2 && 5 < CPS) codes_stage(std::integral_constant<int, (5 < CPS ? 5 : 1)>{}, st, ca); break;
+          case 6: if constexpr (GT <= 4 && 6 < CPS) codes_stage(std::integral_constant<int, (6 < CPS ? 6 : 1)>{}, st, ca); break;
+          case 7: if constexpr (GT <= 2 && 7 < CPS) codes_stage(std::integral_constant<int, (7 < CPS ? 7 : 1)>{}, st, ca); break;
+          default: break;
         }
       } else {
-        // partial stage (end of a slice) or very large groups: step by step
+        // the ragged last group of a layer (m_pad / 128 not a multiple of g / 128): by step
+        const int ga = ca / HG;
         float d[NT][4];
         zero4(d);
-        for (int sidx = 0; sidx < 2 * nck; ++sidx) {
+        for (int s = 0; s < 2 * nck; ++s) {
           uint32_t f[4][4];
-          decode_step(st + (sidx >> 1) * CB, sidx & 1, f);
-          mma_step(f, kc + sidx * 64, d);
-          const int step = 2 * ca + sidx;  // global 64-column step
+          decode_step(st + (s >> 1) * CB, s & 1, f);
+          mma_step(f, ca * 128 + s * 64, d);
+          const int step = 2 * ca + s;
           if ((step % GT) == GT - 1 || step == 2 * a.nch - 1) {
-            const int grp = step / GT;
-            fold(st + kSzOff + (grp - ga) * 64, grp - gx0, d);
+            fold(st + kSzOff + (step / GT - ga) * 64, step / GT, d);
             zero4(d);
           }
         }
       }
     } else {
-      const int wa = sl.w0 + (t - ncs) * kWPS, nwt = min(kWPS, sl.w1 - wa);
+      const int wa = sg.w0 + (t - ncs) * kWPS, nwt = min(kWPS, sg.w1 - wa);
 #pragma unroll
       for (int wt = 0; wt < kWPS; ++wt) {
         if (wt < nwt) {
@@ -412,35 +479,43 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv2_kernel(const G2Args a) {
       slot = 0;
       phase ^= 1u;
     }
-    t += kNW;
+    t += NW;
     while (t >= nst) {
       t -= nst;
       ++jl;
     }
   }
   if (my_n > 0) park(cur_jl);
+  if (tr && threadIdx.x == 0) tr[4] = gtime();
   __syncthreads();
+  if (tr && threadIdx.x == 0) tr[5] = gtime();
   // ---- this CTA's slice partial of every row-block: sum the warps in order (into slot 0) ----
-  for (int e = threadIdx.x; e < nj * redn; e += kNW * 32) {
-    const int jl = e / redn, r = e - jl * redn;
-    const float* p = red + (size_t)jl * kNW * redn + r;
+  for (int e = threadIdx.x; e < nj * redn; e += NW * 32) {
+    const int jq = e / redn, r = e - jq * redn;
+    float* p = red + (size_t)jq * NW * redn + r;
     float v = 0.f;
 #pragma unroll
-    for (int w = 0; w < kNW; ++w) v += p[w * redn];
-    red[(size_t)jl * kNW * redn + r] = v;
+    for (int w = 0; w < NW; ++w) v += p[w * redn];
+    p[0] = v;
   }
   // ---- sum the S slices (ranks in order, over DSMEM) and store y ----
   if (a.S > 1) cluster_sync();
   else __syncthreads();
-  for (int e = threadIdx.x; e < nj * redn; e += kNW * 32) {
-    const int jl = e / redn, r = e - jl * redn;
-    if (a.S > 1 && (jl % a.S) != rank) continue;
-    const uint32_t off = smem_u32(red + (size_t)jl * kNW * redn + r);
-    float v = 0.f;
-    for (int q = 0; q < a.S; ++q) v += a.S > 1 ? ld_dsmem_f32(off, q) : red[(size_t)jl * kNW * redn + r];
-    const int row16 = r / a.n, col = r - row16 * a.n;
+  for (int e = threadIdx.x; e < nj * redn; e += NW * 32) {
+    const int jq = e / redn, r = e - jq * redn;
+    if (a.S > 1 && (jq % a.S) != rank) continue;
+    const float* p = red + (size_t)jq * NW * redn + r;
+    float v;
+    if (a.S > 1) {
+      const uint32_t off = smem_u32(p);
+      v = 0.f;
+      for (int q = 0; q < a.S; ++q) v += ld_dsmem_f32(off, q);
+    } else {
+      v = *p;
+    }
+    const int row16 = ONE ? r : r / n, col = ONE ? 0 : r - row16 * n;
     int lrb;
-    const int l = layer_of(a, j0 + jl, lrb);
+    const int l = layer_of(a, j0 + jq, lrb);
     const int row = lrb * 16 + row16;
     if (row < a.ocs[l]) {
       const int64_t idx = (int64_t)col * a.ldy + row;
@@ -454,19 +529,21 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv2_kernel(const G2Args a) {
     }
   }
   if (a.S > 1) cluster_sync();  // keep this CTA's partials alive until every rank has read them
+  if (tr && threadIdx.x == 0) tr[6] = gtime();
 }
 
 // ---------------------------------------------------------------------------
 // host: slicing and launch
 
-// balance units (codes units then weak tiles) into S contiguous slices by bytes
-void slice_units(int nuc, int U, int nch, int nwt, int cb, int szb, int S, int* ub) {
-  const int nu = nuc + nwt;
+struct Geom {
+  int nch, U, nuc, nwt, cb, szb, m_pad, g, CPS;
+};
+
+// balance units (codes units of U chunks, then weak tiles) into S contiguous slices by bytes
+void slice_units(const Geom& G, int S, int* ub) {
+  const int nu = G.nuc + G.nwt;
   auto ubytes = [&](int u) -> double {
-    if (u < nuc) {
-      const int ch = std::min(U, nch - u * U);
-      return (double)ch * cb + szb;
-    }
+    if (u < G.nuc) return (double)std::min(G.U, G.nch - u * G.U) * G.cb + G.szb;
     return 2048.0;
   };
   double total = 0;
@@ -482,19 +559,39 @@ void slice_units(int nuc, int U, int nch, int nwt, int cb, int szb, int S, int* 
   ub[S] = nu;
 }
 
-int kpos_host(int u, int nuc, int U, int nch, int m_pad) {
-  return u <= nuc ? std::min(u * U, nch) * 128 : m_pad + (u - nuc) * 64;
+SliceGeo slice_geo(const Geom& G, int u0, int u1) {
+  SliceGeo s{};
+  auto kpos = [&](int u) { return u <= G.nuc ? std::min(u * G.U, G.nch) * 128 : G.m_pad + (u - G.nuc) * 64; };
+  s.c0 = std::min(std::min(u0, G.nuc) * G.U, G.nch);
+  s.c1 = std::min(std::min(u1, G.nuc) * G.U, G.nch);
+  s.w0 = std::max(u0, G.nuc) - G.nuc;
+  s.w1 = std::max(u1, G.nuc) - G.nuc;
+  s.kb = kpos(u0);
+  s.ke = kpos(u1);
+  s.gx0 = s.kb < G.m_pad ? s.kb / G.g : 0;
+  s.ngx = s.kb < G.m_pad ? (std::min(s.ke, G.m_pad) - s.gx0 * G.g + G.g - 1) / G.g : 0;
+  s.ncs = (s.c1 - s.c0 + G.CPS - 1) / G.CPS;
+  s.nst = s.ncs + (s.w1 - s.w0 + G.CPS / 2 - 1) / (G.CPS / 2);
+  return s;
 }
 
-template <int BITS, int NT, int GT, typename T, int R, int NW, int CPS>
-int launch2(G2Args a, const qeft_linear_t* L, cudaStream_t st) {
-  constexpr int kNW = NW, kStage = CPS * 1152;
-  auto kern = gemv2_kernel<BITS, NT, GT, T, R, NW, CPS>;
-  constexpr int kSmemMax = 227 * 1024 - 1024;
+// MINB CTAs per SM (2: a CTA of the next launch can start -- and prefetch its weights --
+// beside a CTA of this one)
+template <int BITS, int NT, int GT, typename T, int R, int NW, int CPS, int MINB = 1>
+int launch2(G2Args a, cudaStream_t st) {
+  constexpr int kStage = CPS * 1152;
+  constexpr int kSmemMax = (MINB == 1 ? 227 * 1024 : 113 * 1024) - 1024;
+  constexpr int PRE = MINB > 1 ? R : 0;  // pre-wait weight prefetch only when CTAs can overlap
+  auto kern1 = gemv2_kernel<BITS, NT, GT, T, R, NW, CPS, true, MINB, PRE>;
+  auto kernN = gemv2_kernel<BITS, NT, GT, T, R, NW, CPS, false, MINB, PRE>;
+  const bool one = a.n == 1 && NT == 1;
+  auto kern = one ? kern1 : kernN;
   static bool attr = false;
   if (!attr) {
-    QEFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-    QEFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    for (auto kk : {kern1, kernN}) {
+      QEFT_CUDA(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+      QEFT_CUDA(cudaFuncSetAttribute(kk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    }
     attr = true;
   }
   static int sms = 0;
@@ -503,10 +600,17 @@ int launch2(G2Args a, const qeft_linear_t* L, cudaStream_t st) {
     QEFT_CUDA(cudaGetDevice(&dev));
     QEFT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  const int cb = BITS == 4 ? 1024 : 768;
-  const int szb = 64 * std::max(1, a.U * 128 / a.g);
-  const int nwt = a.k_pad / 64;
-  const int rings = kNW * R * kStage;
+  Geom G;
+  G.nch = a.nch;
+  G.U = std::max(1, a.g / 128);
+  G.nuc = (G.nch + G.U - 1) / G.U;
+  G.nwt = a.k_pad / 64;
+  G.cb = BITS == 4 ? 1024 : 768;
+  G.szb = 64 * std::max(1, G.U * 128 / a.g);
+  G.m_pad = a.m_pad;
+  G.g = a.g;
+  G.CPS = CPS;
+  const int rings = NW * R * kStage;
   const int force_s = env_int("QEFT_GEMV2_S", 0);
   // choose the cluster size S (= K slices): the busiest CTA streams J row-blocks of its slice
   double best = 1e300;
@@ -515,59 +619,58 @@ int launch2(G2Args a, const qeft_linear_t* L, cudaStream_t st) {
   size_t best_smem = 0;
   for (int S = 1; S <= kMaxS; ++S) {
     if (force_s && S != force_s) continue;
-    if (S > a.nuc + nwt) break;
+    if (S > G.nuc + G.nwt) break;
     G2Args b = a;
     b.S = S;
-    slice_units(a.nuc, a.U, a.nch, nwt, cb, szb, S, b.ub);
+    int ub[kMaxS + 1];
+    slice_units(G, S, ub);
     bool empty = false;
     double smax = 0;
     int xc = 0, xg = 0;
     for (int s = 0; s < S; ++s) {
-      empty |= b.ub[s + 1] == b.ub[s];
-      const int kb = kpos_host(b.ub[s], a.nuc, a.U, a.nch, a.m_pad), ke = kpos_host(b.ub[s + 1], a.nuc, a.U, a.nch, a.m_pad);
-      xc = std::max(xc, ke - kb);
-      if (kb < a.m_pad) xg = std::max(xg, (std::min(ke, a.m_pad) - kb / a.g * a.g + a.g - 1) / a.g);
-      const int c0 = std::min(std::min(b.ub[s], a.nuc) * a.U, a.nch), c1 = std::min(std::min(b.ub[s + 1], a.nuc) * a.U, a.nch);
-      const int w0 = std::max(b.ub[s], a.nuc) - a.nuc, w1 = std::max(b.ub[s + 1], a.nuc) - a.nuc;
-      smax = std::max(smax, (double)(c1 - c0) * cb + (double)(c1 - c0) * 128 / a.g * 64 + (w1 - w0) * 2048.0);
+      empty |= ub[s + 1] == ub[s];
+      b.geo[s] = slice_geo(G, ub[s], ub[s + 1]);
+      const SliceGeo& q = b.geo[s];
+      xc = std::max(xc, q.ke - q.kb);
+      xg = std::max(xg, q.ngx);
+      smax = std::max(smax, (double)(q.c1 - q.c0) * G.cb + (double)(q.c1 - q.c0) * 128 / a.g * 64 +
+                                (q.w1 - q.w0) * 2048.0);
     }
     if (empty) continue;
     b.xs_ld = xc + 8;  // 16 B skew between staged x rows
     // clusters that fit on the GPU at once (persistent: one wave)
-    int nclu = sms / S;
+    int nclu = sms * MINB / S;
     size_t smem = 0;
     for (int it = 0; it < 3; ++it) {
       b.J = (a.n_rb + nclu - 1) / nclu;
       if (b.J > kMaxJ) break;
-      smem = (size_t)rings + (size_t)b.J * kNW * 16 * a.n * 4 + (size_t)a.n * b.xs_ld * 2 + (size_t)xg * NT * 8 * 4;
+      smem = (size_t)rings + (size_t)b.J * NW * 16 * a.n * 4 + (size_t)a.n * b.xs_ld * 2 + (size_t)xg * NT * 8 * 4;
       if (smem > (size_t)kSmemMax) break;
-      if (S > 1) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(nclu * S);
-        cfg.blockDim = dim3(kNW * 32);
-        cfg.dynamicSmemBytes = smem;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = S;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        int maxc = 0;
-        if (cudaOccupancyMaxActiveClusters(&maxc, kern, &cfg) != cudaSuccess || maxc <= 0) {
-          cudaGetLastError();
-          smem = 0;
-          break;
-        }
-        if (maxc >= nclu) break;
-        nclu = maxc;
-      } else {
+      if (S == 1) break;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(nclu * S);
+      cfg.blockDim = dim3(NW * 32);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = S;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int maxc = 0;
+      if (cudaOccupancyMaxActiveClusters(&maxc, kern, &cfg) != cudaSuccess || maxc <= 0) {
+        cudaGetLastError();
+        smem = 0;
         break;
       }
+      if (maxc >= nclu) break;
+      nclu = maxc;
     }
     if (b.J > kMaxJ || smem == 0 || smem > (size_t)kSmemMax) continue;
     const int ncl = (a.n_rb + b.J - 1) / b.J;
-    const double cost = b.J * smax + (S > 1 ? 8192.0 : 0.0);  // + the DSMEM reduction
+    // + the cluster epilogue (~1.6 us measured, i.e. ~70 KB of one SM's HBM share)
+    const double cost = b.J * smax + (S > 1 ? 70.0 * 1024 : 0.0);
     if (cost < best * 0.98) {
       best = cost;
       bestA = b;
@@ -577,34 +680,36 @@ int launch2(G2Args a, const qeft_linear_t* L, cudaStream_t st) {
   }
   if (best_grid == 0) return -1;  // partials do not fit shared memory: the generic kernel serves it
   if (bestA.S > 1) {
-    QEFT_CUDA(launch_pdl_cluster(kern, dim3(best_grid), dim3(kNW * 32), best_smem, st, bestA.S, bestA));
+    QEFT_CUDA(launch_pdl_cluster(kern, dim3(best_grid), dim3(NW * 32), best_smem, st, bestA.S, bestA));
   } else {
-    QEFT_CUDA(launch_pdl(kern, dim3(best_grid), dim3(kNW * 32), best_smem, st, bestA));
+    QEFT_CUDA(launch_pdl(kern, dim3(best_grid), dim3(NW * 32), best_smem, st, bestA));
   }
   return 0;
 }
 
 template <int BITS, typename T>
-int dispatch2(const G2Args& a, const qeft_linear_t* L, int gt, cudaStream_t st) {
+int dispatch2(const G2Args& a, int gt, cudaStream_t st) {
   const bool nt2 = a.n > 8;
   if constexpr (BITS == 4 && std::is_same<T, __half>::value) {
     // tuning variants of the 7B decode path (4-bit, g = 128, <= 8 columns)
     static const int var = env_int("QEFT_GEMV2_VAR", 0);
     if (!nt2 && gt == 2 && var) {
       switch (var) {
-        case 1: return launch2<4, 1, 2, T, 2, 16, 4>(a, L, st);
-        case 2: return launch2<4, 1, 2, T, 2, 8, 8>(a, L, st);
-        case 3: return launch2<4, 1, 2, T, 2, 12, 4>(a, L, st);
+        case 1: return launch2<4, 1, 2, T, 3, 8, 4>(a, st);
+        case 2: return launch2<4, 1, 2, T, 2, 8, 8>(a, st);
+        case 3: return launch2<4, 1, 2, T, 2, 12, 4>(a, st);
+        case 4: return launch2<4, 1, 2, T, 2, 8, 4, 2>(a, st);
+        case 5: return launch2<4, 1, 2, T, 2, 16, 4, 1>(a, st);
         default: break;
       }
     }
   }
-#define QEFT_G2(NT)                                                  \
-  switch (gt) {                                                      \
-    case 1: return launch2<BITS, NT, 1, T, 3, 8, 4>(a, L, st);       \
-    case 2: return launch2<BITS, NT, 2, T, 3, 8, 4>(a, L, st);       \
-    case 4: return launch2<BITS, NT, 4, T, 3, 8, 4>(a, L, st);       \
-    default: return launch2<BITS, NT, 8, T, 3, 8, 4>(a, L, st);      \
+#define QEFT_G2(NT)                                            \
+  switch (gt) {                                                \
+    case 1: return launch2<BITS, NT, 1, T, 2, 16, 4>(a, st);   \
+    case 2: return launch2<BITS, NT, 2, T, 2, 16, 4>(a, st);   \
+    case 4: return launch2<BITS, NT, 4, T, 2, 16, 4>(a, st);   \
+    default: return launch2<BITS, NT, 8, T, 2, 16, 4>(a, st);  \
   }
   if (nt2) {
     QEFT_G2(2)
@@ -626,6 +731,31 @@ bool gemv2_supported(const qeft_linear_t* L, int n) {
 }
 
 size_t gemv2_workspace_bytes(const qeft_linear_t*, int) { return 0; }
+
+// profiling: per-CTA timestamps of the next launches (8 per CTA, 512 CTAs per launch slot)
+static unsigned long long* g_trace = nullptr;
+static int g_trace_slots = 0, g_trace_next = 0;
+constexpr int kTraceCtas = 512;
+
+int gemv_trace(int slots, unsigned long long* host_out) {
+  if (slots > 0) {  // arm: allocate and clear
+    if (g_trace) cudaFree(g_trace);
+    QEFT_CUDA(cudaMalloc(&g_trace, (size_t)slots * kTraceCtas * 8 * sizeof(unsigned long long)));
+    QEFT_CUDA(cudaMemset(g_trace, 0, (size_t)slots * kTraceCtas * 8 * sizeof(unsigned long long)));
+    g_trace_slots = slots;
+    g_trace_next = 0;
+    return 0;
+  }
+  if (host_out && g_trace) {
+    QEFT_CUDA(cudaDeviceSynchronize());
+    QEFT_CUDA(cudaMemcpy(host_out, g_trace, (size_t)g_trace_slots * kTraceCtas * 8 * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost));
+  }
+  if (g_trace) cudaFree(g_trace);
+  g_trace = nullptr;
+  g_trace_slots = 0;
+  return 0;
+}
 
 int gemv2_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ldx, void* const* ys, int64_t ldy,
                 int y_f32, int n, void*, size_t, cudaStream_t st) {
@@ -658,14 +788,14 @@ int gemv2_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t l
   a.n = n;
   a.n_rb = rb_total;
   a.nch = L->m_pad / 128;
-  a.U = std::max(1, L->g / 128);
-  a.nuc = (a.nch + a.U - 1) / a.U;
   a.ng16 = (L->m_pad + L->g - 1) / L->g;
   a.rbb = rowblock_bytes(L->bits, L->m_pad);
+  a.trace = nullptr;
+  if (g_trace && g_trace_next < g_trace_slots) a.trace = g_trace + (size_t)(g_trace_next++) * kTraceCtas * 8;
   const int gt = L->g / 64;
   const bool bf = L->act_dtype == QEFT_BF16;
-  if (L->bits == 4) return bf ? dispatch2<4, __nv_bfloat16>(a, L, gt, st) : dispatch2<4, __half>(a, L, gt, st);
-  return bf ? dispatch2<3, __nv_bfloat16>(a, L, gt, st) : dispatch2<3, __half>(a, L, gt, st);
+  if (L->bits == 4) return bf ? dispatch2<4, __nv_bfloat16>(a, gt, st) : dispatch2<4, __half>(a, gt, st);
+  return bf ? dispatch2<3, __nv_bfloat16>(a, gt, st) : dispatch2<3, __half>(a, gt, st);
 }
 
 }  // namespace qeft

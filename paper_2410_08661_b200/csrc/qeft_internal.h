@@ -56,6 +56,7 @@ int gemv_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ld
                int y_f32, int n, void* ws, size_t ws_bytes, cudaStream_t st);
 // bulk-copy warp-ring GEMV (qeft_gemv2.cu); gemv2_multi returns -1 when the launch needs the
 // generic path (its partials would not fit shared memory)
+int gemv_trace(int slots, unsigned long long* host_out);
 bool gemv2_supported(const qeft_linear_t* L, int n);
 size_t gemv2_workspace_bytes(const qeft_linear_t* L, int n);
 int gemv2_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ldx, void* const* ys,

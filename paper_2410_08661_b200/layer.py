@@ -215,7 +215,7 @@ class DeviceLayer:
             out = torch.empty((T, self.oc), dtype=self.tdtype, device=x.device)
         L = _lib.lib()
         ws = WORKSPACE.get(int(L.qeft_gemm_workspace_bytes(self.cptr, T)), x.device)
-        _lib.check(L.qeft_gemm_fwd(self.cptr, _lib.ptr(x), x.stride(0), _lib.ptr(out), out.stride(0),
+        _lib.check(L.qeft_gemm_fwd(self.cptr, _lib.ptr(x), _ld(x), _lib.ptr(out), _ld(out),
                                    T, _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "gemm_fwd")
         return out
 
@@ -233,8 +233,8 @@ class DeviceLayer:
             accumulate = False
         L = _lib.lib()
         ws = WORKSPACE.get(int(L.qeft_gemm_workspace_bytes(self.cptr, T)), dy.device)
-        _lib.check(L.qeft_gemm_dgrad(self.cptr, _lib.ptr(dy), dy.stride(0), _lib.ptr(out),
-                                     out.stride(0), T, int(accumulate), _lib.ptr(ws), ws.numel(),
+        _lib.check(L.qeft_gemm_dgrad(self.cptr, _lib.ptr(dy), _ld(dy), _lib.ptr(out),
+                                     _ld(out), T, int(accumulate), _lib.ptr(ws), ws.numel(),
                                      _lib.stream_ptr()), "gemm_dgrad")
         return out
 
@@ -250,7 +250,7 @@ class DeviceLayer:
             out = torch.empty((T, kw), dtype=x.dtype, device=x.device)
         if self.k:
             _lib.check(_lib.lib().qeft_gather_cols(
-                _lib.ptr(x), x.stride(0), self.colmap.data_ptr() + 4 * self.m_pad, kw, T,
+                _lib.ptr(x), _ld(x), self.colmap.data_ptr() + 4 * self.m_pad, kw, T,
                 _DT[self.dtype], _lib.ptr(out), _lib.stream_ptr()), "gather_weak")
         return out
 
@@ -267,8 +267,8 @@ class DeviceLayer:
             return out
         L = _lib.lib()
         ws = WORKSPACE.get(int(L.qeft_gemm_workspace_bytes(self.cptr, T)), dy.device)
-        _lib.check(L.qeft_gemm_wgrad_weak(self.cptr, _lib.ptr(dy), dy.stride(0), _lib.ptr(x_weak),
-                                          x_weak.stride(0), _lib.ptr(out), T, int(accumulate),
+        _lib.check(L.qeft_gemm_wgrad_weak(self.cptr, _lib.ptr(dy), _ld(dy), _lib.ptr(x_weak),
+                                          _ld(x_weak), _lib.ptr(out), T, int(accumulate),
                                           _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "gemm_wgrad_weak")
         return out
 
@@ -285,10 +285,15 @@ class DeviceLayer:
             accumulate = False
         L = _lib.lib()
         ws = WORKSPACE.get(int(L.qeft_gemm_workspace_bytes(self.cptr, T)), dy.device)
-        _lib.check(L.qeft_gemm_wgrad(self.cptr, _lib.ptr(dy), dy.stride(0), _lib.ptr(x), x.stride(0),
+        _lib.check(L.qeft_gemm_wgrad(self.cptr, _lib.ptr(dy), _ld(dy), _lib.ptr(x), _ld(x),
                                      _lib.ptr(out), T, int(accumulate), _lib.ptr(ws), ws.numel(),
                                      _lib.stream_ptr()), "gemm_wgrad")
         return out
+
+
+def _ld(t) -> int:
+    """Row pitch of a row-major 2-D tensor; a single row may carry any stride(0)."""
+    return t.stride(0) if t.shape[0] > 1 else t.shape[1]
 
 
 def _source_id(q):
