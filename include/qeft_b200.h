@@ -170,7 +170,7 @@ int qeft_div_scalar(float* g, int64_t n, float divisor, void* stream);
  * c_b1 = f32(b1), c_1mb1 = f32(1-b1), c_b2, c_1mb2, bc1 = f32(1-b1**t),
  * bc2 = f32(1-b2**t). max_norm <= 0 disables clipping. */
 int qeft_adam_clip(float* w32, float* m, float* v, const float* g, int64_t n, const double* sqnorm,
-                   float max_norm, float lr, float c_b1, float c_1mb1, float c_b2, float c_1mb2,
+                   double max_norm, float lr, float c_b1, float c_1mb1, float c_b2, float c_1mb2,
                    float bc1, float bc2, float eps, int* nonfinite_flag, void* stream);
 /* Refresh the weak16 shadows from the fp32 masters after the update.
  * descs: device array of n_layers {int64 offset, int32 oc, k, k_pad, dtype, ptr}. */
@@ -181,6 +181,17 @@ typedef struct qeft_shadow_desc {
 } qeft_shadow_desc_t;
 int qeft_weak_shadow(const float* w32, const qeft_shadow_desc_t* descs, int n_layers, int max_elems,
                      void* stream);
+/* The fine-tune step's optimizer in two passes over the flat bucket (tuning.py:226-236):
+ *   qeft_grad_sqnorm_div: out = sum((g / divisor)^2) in fp64, g / divisor rounded to fp32 first
+ *                         (the reference's acc /= grad_accum, then the fp64 norm);
+ *   qeft_adam_step_flat:  per element of every layer in descs: g / divisor -> global clip (from
+ *                         *sqnorm, max_norm a double) -> fp32 Adam on w32/m/v -> weak16 shadow.
+ *                         max_rows = the largest oc among the layers. g is not modified. */
+int qeft_grad_sqnorm_div(const float* g, int64_t n, float divisor, double* scratch, double* out, void* stream);
+int qeft_adam_step_flat(float* w32, float* m, float* v, const float* g, const qeft_shadow_desc_t* descs,
+                        int n_layers, int max_rows, float divisor, const double* sqnorm, double max_norm,
+                        float lr, float c_b1, float c_1mb1, float c_b2, float c_1mb2, float bc1, float bc2,
+                        float eps, int* nonfinite_flag, void* stream);
 
 /* ---- fused elementwise ops of the fine-tuning host model (model.py:249-275, 389-391) ----
  * Activations row-major fp16/bf16 (dt), fp32 math; gains frozen (tuning.py: param_grads=False).

@@ -63,7 +63,11 @@ SIGNATURES = {
     "qeft_gemm_wgrad_weak": (_I, [_LP, _VP, _I64, _VP, _I64, _VP, _I, _I, _VP, _SZ, _VP]),
     "qeft_grad_sqnorm": (_I, [_VP, _I64, _VP, _VP, _VP]),
     "qeft_div_scalar": (_I, [_VP, _I64, _F, _VP]),
-    "qeft_adam_clip": (_I, [_VP, _VP, _VP, _VP, _I64, _VP, _F, _F, _F, _F, _F, _F, _F, _F, _F, _VP, _VP]),
+    "qeft_adam_clip": (_I, [_VP, _VP, _VP, _VP, _I64, _VP, ctypes.c_double, _F, _F, _F, _F, _F, _F, _F, _F, _VP,
+                            _VP]),
+    "qeft_grad_sqnorm_div": (_I, [_VP, _I64, _F, _VP, _VP, _VP]),
+    "qeft_adam_step_flat": (_I, [_VP, _VP, _VP, _VP, _VP, _I, _I, _F, _VP, ctypes.c_double, _F, _F, _F, _F, _F,
+                                 _F, _F, _F, _VP, _VP]),
     "qeft_weak_shadow": (_I, [_VP, _VP, _I, _I, _VP]),
     "qeft_rmsnorm_fwd": (_I, [_VP, _VP, _VP, _VP, _I, _I, _I, _VP]),
     "qeft_rmsnorm_bwd": (_I, [_VP, _VP, _VP, _VP, _VP, _VP, _I, _I, _I, _VP]),

@@ -1,9 +1,13 @@
-"""Weak-column selection (bit-exact index contract).
+"""Calibration statistics and weak-column selection.
 
-Host-side integer work, restated from pkg/src/qeft/calibration.py:73-187 with
-identical numpy semantics (stable argsort, lower index wins ties, fp64 score
-accumulation in trace order). It runs once per model offline; there is
-nothing here worth a kernel.
+* HessianFull / accumulate_hessian_full (calibration.py:101-122): the per-layer running mean
+  of 2 X X^T over calibration sequences, the input of OPTQ error compensation. Computed on
+  the GPU: X^T X is a plain fp64 GEMM (cuBLAS DGEMM through torch -- products of fp32 values
+  are exact in fp64, so only the summation order differs from the reference's BLAS call),
+  and the running mean is updated in place on the device, (prev * n + c) / (n + 1) in fp64.
+* selection (calibration.py:73-187): host-side integer work with identical numpy semantics
+  (stable argsort, lower index wins ties, fp64 score accumulation in trace order); it runs
+  once per model offline, so there is nothing there worth a kernel.
 """
 
 from __future__ import annotations
@@ -23,6 +27,56 @@ class HessianDiag:
     """Per-layer lambda = running mean of 2*sum_t X^2 (calibration.py:60-64)."""
     lam: dict
     sample_count: int = 0
+
+
+@dataclass
+class HessianFull:
+    """calibration.py:101-110: full 2 X X^T running means per layer (name -> IC x IC fp64,
+    CUDA tensors; `numpy()` gives the host dict), in trace (insertion) order."""
+    h: dict
+    sample_count: int = 0
+
+    def diag(self) -> HessianDiag:
+        """lambda = the diagonals (calibration.py:107-110), as host fp64 arrays."""
+        return HessianDiag(lam={k: _host(v).diagonal().copy() if not hasattr(v, "is_cuda")
+                                else v.diagonal().cpu().numpy().copy() for k, v in self.h.items()},
+                           sample_count=self.sample_count)
+
+    def numpy(self) -> dict:
+        return {k: _host(v) for k, v in self.h.items()}
+
+
+def _host(v):
+    return v.cpu().numpy() if hasattr(v, "is_cuda") else np.asarray(v, np.float64)
+
+
+def accumulate_hessian_full(trace, running: HessianFull | None = None, device=None) -> HessianFull:
+    """calibration.py:113-122: fold one traced call (an object with `.activations`, or a dict
+    name -> (IC, tokens) activations, numpy or CUDA) into the running mean of 2 X X^T, on the
+    GPU in fp64."""
+    import torch
+    acts = trace.activations if hasattr(trace, "activations") else trace
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    contrib = {}
+    for name, x in acts.items():
+        xd = (x if hasattr(x, "is_cuda") else torch.from_numpy(np.ascontiguousarray(x))).to(
+            dev, dtype=torch.float64)
+        if xd.dim() != 2:
+            raise ShapeError(f"layer {name}: activations must be (IC, tokens)")
+        contrib[name] = torch.matmul(xd, xd.T).mul_(2.0)
+    if running is None:
+        return HessianFull(h=contrib, sample_count=1)
+    if set(running.h) != set(contrib):
+        raise ShapeError("trace layer set does not match running state")
+    n = running.sample_count
+    h = {}
+    for name, c in contrib.items():
+        prev = running.h[name]
+        prev = prev if hasattr(prev, "is_cuda") else torch.from_numpy(np.asarray(prev, np.float64)).to(dev)
+        if prev.shape != c.shape:
+            raise ShapeError(f"layer {name}: IC {c.shape[0]} does not match running {prev.shape[0]}")
+        h[name] = (prev * n + c) / (n + 1)
+    return HessianFull(h=h, sample_count=n + 1)
 
 
 @dataclass

@@ -152,10 +152,23 @@ int qeft_grad_sqnorm(const float* g, int64_t n, double* scratch, double* out, vo
 int qeft_div_scalar(float* g, int64_t n, float d, void* s) { return div_scalar(g, n, d, ST(s)); }
 
 int qeft_adam_clip(float* w, float* m, float* v, const float* g, int64_t n, const double* sq,
-                   float max_norm, float lr, float c_b1, float c_1mb1, float c_b2, float c_1mb2,
+                   double max_norm, float lr, float c_b1, float c_1mb1, float c_b2, float c_1mb2,
                    float bc1, float bc2, float eps, int* flag, void* s) {
   return adam_clip(w, m, v, g, n, sq, max_norm, lr, c_b1, c_1mb1, c_b2, c_1mb2, bc1, bc2, eps, flag,
                    ST(s));
+}
+
+int qeft_grad_sqnorm_div(const float* g, int64_t n, float divisor, double* scratch, double* out, void* s) {
+  QEFT_CHECK(divisor != 0.f, QEFT_ERR_SHAPE, "grad_sqnorm_div: zero divisor");
+  return grad_sqnorm(g, n, scratch, out, ST(s), divisor);
+}
+
+int qeft_adam_step_flat(float* w32, float* m, float* v, const float* g, const qeft_shadow_desc_t* descs,
+                        int n_layers, int max_rows, float divisor, const double* sq, double max_norm, float lr,
+                        float c_b1, float c_1mb1, float c_b2, float c_1mb2, float bc1, float bc2, float eps,
+                        int* flag, void* s) {
+  return adam_step_flat(w32, m, v, g, descs, n_layers, max_rows, divisor, sq, max_norm, lr, c_b1, c_1mb1, c_b2,
+                        c_1mb2, bc1, bc2, eps, flag, ST(s));
 }
 
 int qeft_weak_shadow(const float* w32, const qeft_shadow_desc_t* d, int n, int max_elems, void* s) {

@@ -233,6 +233,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
         xs[r * a.xs_ld + (c < nz0 ? z0a + c : z1a + c - nz0) - kb] = zero;
       }
       mbar_wait(&xbar, 0);
+      if (tr && threadIdx.x == 0) tr[5] = gtime();
     } else {
       if (lane == 0)
         while (issued < R && issue(false)) {
@@ -488,7 +489,6 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
   if (my_n > 0) park(cur_jl);
   if (tr && threadIdx.x == 0) tr[4] = gtime();
   __syncthreads();
-  if (tr && threadIdx.x == 0) tr[5] = gtime();
   // ---- this CTA's slice partial of every row-block: sum the warps in order (into slot 0) ----
   for (int e = threadIdx.x; e < nj * redn; e += NW * 32) {
     const int jq = e / redn, r = e - jq * redn;
@@ -577,7 +577,7 @@ SliceGeo slice_geo(const Geom& G, int u0, int u1) {
 
 // MINB CTAs per SM (2: a CTA of the next launch can start -- and prefetch its weights --
 // beside a CTA of this one)
-template <int BITS, int NT, int GT, typename T, int R, int NW, int CPS, int MINB = 1>
+template <int BITS, int NT, int GT, typename T, int R, int NW, int CPS, int MINB = 1, int GPS = MINB>
 int launch2(G2Args a, cudaStream_t st) {
   constexpr int kStage = CPS * 1152;
   constexpr int kSmemMax = (MINB == 1 ? 227 * 1024 : 113 * 1024) - 1024;
@@ -639,7 +639,7 @@ int launch2(G2Args a, cudaStream_t st) {
     if (empty) continue;
     b.xs_ld = xc + 8;  // 16 B skew between staged x rows
     // clusters that fit on the GPU at once (persistent: one wave)
-    int nclu = sms * MINB / S;
+    int nclu = sms * GPS / S;
     size_t smem = 0;
     for (int it = 0; it < 3; ++it) {
       b.J = (a.n_rb + nclu - 1) / nclu;
@@ -700,21 +700,26 @@ int dispatch2(const G2Args& a, int gt, cudaStream_t st) {
         case 3: return launch2<4, 1, 2, T, 2, 12, 4>(a, st);
         case 4: return launch2<4, 1, 2, T, 2, 8, 4, 2>(a, st);
         case 5: return launch2<4, 1, 2, T, 2, 16, 4, 1>(a, st);
+        case 6: return launch2<4, 1, 2, T, 2, 8, 4, 2, 1>(a, st);
         default: break;
       }
     }
   }
-#define QEFT_G2(NT)                                            \
-  switch (gt) {                                                \
-    case 1: return launch2<BITS, NT, 1, T, 2, 16, 4>(a, st);   \
-    case 2: return launch2<BITS, NT, 2, T, 2, 16, 4>(a, st);   \
-    case 4: return launch2<BITS, NT, 4, T, 2, 16, 4>(a, st);   \
-    default: return launch2<BITS, NT, 8, T, 2, 16, 4>(a, st);  \
+#define QEFT_G2(NT, NWV)                                         \
+  switch (gt) {                                                  \
+    case 1: return launch2<BITS, NT, 1, T, 2, NWV, 4>(a, st);    \
+    case 2: return launch2<BITS, NT, 2, T, 2, NWV, 4>(a, st);    \
+    case 4: return launch2<BITS, NT, 4, T, 2, NWV, 4>(a, st);    \
+    default: return launch2<BITS, NT, 8, T, 2, NWV, 4>(a, st);   \
   }
+  // batch-1/2 decode: 16 warps (the decode + MMA issue rate is the limit); wider batches: 8
+  // warps, so the per-warp partials and the staged x of several columns fit shared memory
   if (nt2) {
-    QEFT_G2(2)
+    QEFT_G2(2, 8)
+  } else if (a.n > 2) {
+    QEFT_G2(1, 8)
   } else {
-    QEFT_G2(1)
+    QEFT_G2(1, 16)
   }
 #undef QEFT_G2
 }

@@ -71,10 +71,14 @@ int gemm_wgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, const void*
                float* dw, int T, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st,
                bool x_is_weak = false);
 
-int grad_sqnorm(const float* g, int64_t n, double* scratch, double* out, cudaStream_t st);
+int grad_sqnorm(const float* g, int64_t n, double* scratch, double* out, cudaStream_t st, float div = 1.f);
 int div_scalar(float* g, int64_t n, float d, cudaStream_t st);
+int adam_step_flat(float* w, float* m, float* v, const float* g, const qeft_shadow_desc_t* descs, int n_layers,
+                   int max_rows, float div, const double* sqnorm, double max_norm, float lr, float c_b1,
+                   float c_1mb1, float c_b2, float c_1mb2, float bc1, float bc2, float eps, int* flag,
+                   cudaStream_t st);
 int adam_clip(float* w, float* m, float* v, const float* g, int64_t n, const double* sqnorm,
-              float max_norm, float lr, float c_b1, float c_1mb1, float c_b2, float c_1mb2, float bc1,
+              double max_norm, float lr, float c_b1, float c_1mb1, float c_b2, float c_1mb2, float bc1,
               float bc2, float eps, int* flag, cudaStream_t st);
 int weak_shadow(const float* w32, const qeft_shadow_desc_t* d, int n_layers, int max_elems,
                 cudaStream_t st);

@@ -83,7 +83,7 @@ def adam_clip_(w, m, v, g, step: int, lr, *, max_norm=0.0, beta1=0.9, beta2=0.99
     c = adam_constants(step, lr, beta1, beta2, eps)
     _lib.check(_lib.lib().qeft_adam_clip(
         _lib.ptr(w), _lib.ptr(m), _lib.ptr(v), _lib.ptr(g), g.numel(), _lib.ptr(sqnorm),
-        _f32(max_norm or 0.0), c["lr"], c["c_b1"], c["c_1mb1"], c["c_b2"], c["c_1mb2"], c["bc1"],
+        float(max_norm or 0.0), c["lr"], c["c_b1"], c["c_1mb1"], c["c_b2"], c["c_1mb2"], c["bc1"],
         c["bc2"], c["eps"], _lib.ptr(flag), _lib.stream_ptr()), "adam_clip")
     return flag
 
@@ -102,6 +102,25 @@ def adam_step(state: AdamState, w, grad, lr, beta1=0.9, beta2=0.999, eps=1e-8):
         state.step -= 1
         raise DivergenceError("non-finite gradient in adam_step")
     return w
+
+
+def grad_sqnorm_div(g, divisor: float, out):
+    """out = sum((g / divisor)^2), fp64, g / divisor rounded to fp32 first (tuning.py:228-230)."""
+    scratch, _, _ = _SCRATCH.get(g.device)
+    _lib.check(_lib.lib().qeft_grad_sqnorm_div(_lib.ptr(g), g.numel(), _f32(divisor), _lib.ptr(scratch),
+                                               _lib.ptr(out), _lib.stream_ptr()), "grad_sqnorm_div")
+    return out
+
+
+def adam_step_flat(w, m, v, g, descs, n_layers, max_rows, divisor, step, lr, *, max_norm, sqnorm, flag,
+                   beta1=0.9, beta2=0.999, eps=1e-8):
+    """One fused pass: g / divisor -> global clip -> fp32 Adam -> weak16 shadows."""
+    c = adam_constants(step, lr, beta1, beta2, eps)
+    _lib.check(_lib.lib().qeft_adam_step_flat(
+        _lib.ptr(w), _lib.ptr(m), _lib.ptr(v), _lib.ptr(g), _lib.ptr(descs), n_layers, max_rows, _f32(divisor),
+        _lib.ptr(sqnorm), float(max_norm or 0.0), c["lr"], c["c_b1"], c["c_1mb1"], c["c_b2"], c["c_1mb2"],
+        c["bc1"], c["bc2"], c["eps"], _lib.ptr(flag), _lib.stream_ptr()), "adam_step_flat")
+    return flag
 
 
 def shadow_descs(layers, offsets):

@@ -55,6 +55,8 @@ class _QEFTLinearFn(torch.autograd.Function):
             # accumulate straight into the (bucket-backed) .grad: micro-batches add up
             # exactly like the reference's acc[name] += grads[name] (tuning.py:219-224)
             dl.gemm_wgrad_weak(dy, xw, out=w.grad, accumulate=True)
+            if mod.grad_ready_hook is not None:  # e.g. launch this layer group's DP all-reduce
+                mod.grad_ready_hook(mod)
         return dx, None, None
 
 
@@ -68,9 +70,13 @@ class QEFTLinear(torch.nn.Module):
         self.oc, self.ic, self.k = dl.oc, dl.ic, dl.k
         w = dl.weak32
         if w is None:
-            # synthetic layers carry only the kernel copy; the master is read back from it
-            w = dl.dequant_full()[:, _weak_columns(dl)].contiguous()
+            # synthetic layers carry only the kernel copy: untile weak16 ([oc_pad/16][k_pad/64]
+            # tiles of 16 x 64, csrc/qeft_common.cuh weak_off) into the fp32 master
+            kp = dl.k_pad
+            w = (dl.weak16.reshape(dl.oc_pad // 16, kp // 64, 16, 64).permute(0, 2, 1, 3)
+                 .reshape(dl.oc_pad, kp)[:dl.oc, :dl.k].float().contiguous())
         self.weak32 = torch.nn.Parameter(w.reshape(dl.oc, dl.k).float(), requires_grad=trainable)
+        self.grad_ready_hook = None  # called after this layer's dW_weak lands in .grad
 
     @classmethod
     def from_quantized(cls, q, dtype="bf16", name="", trainable=True):

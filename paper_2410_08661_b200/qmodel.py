@@ -10,7 +10,11 @@ reads are required; everything else is carried through untouched.
 from __future__ import annotations
 
 import copy
+import hashlib
+import json
 from dataclasses import dataclass, field
+
+import numpy as np
 
 from .errors import ConfigError
 
@@ -49,6 +53,44 @@ LLAMA2_7B = ModelConfig(d_model=4096, n_heads=32, head_dim=128, d_ff=11008, n_bl
                         vocab_size=32000, max_seq=2048)
 LLAMA2_13B = ModelConfig(d_model=5120, n_heads=40, head_dim=128, d_ff=13824, n_blocks=40,
                          vocab_size=32000, max_seq=2048)
+
+
+@dataclass
+class DenseBlock:
+    """model.py:66-80 BlockWeights: one decoder block's fp32 weights ((out, in) matrices)."""
+    gain1: object
+    wq: object
+    wk: object
+    wv: object
+    wo: object
+    gain2: object
+    w_up: object
+    w_gate: object
+    w_down: object
+
+
+@dataclass
+class DenseModel:
+    """model.py:83-99: the dense fp32 model quantize_model starts from (any object with these
+    fields -- the reference's own DenseModel included -- is accepted)."""
+    config: ModelConfig
+    embedding: object
+    blocks: list
+    final_gain: object
+    head: object
+
+    def copy(self) -> "DenseModel":
+        return copy.deepcopy(self)
+
+
+REORDER_MODES = ("ogr", "online", "none")  # qmodel.py:38
+
+
+def model_fingerprint(config) -> str:
+    """qmodel.py:74-79: architecture hash; same-shape models match regardless of weights."""
+    arch = {f: getattr(config, f) for f in
+            ("d_model", "n_heads", "head_dim", "d_ff", "n_blocks", "vocab_size", "max_seq")}
+    return hashlib.sha256(json.dumps(arch, sort_keys=True).encode()).hexdigest()[:16]
 
 
 @dataclass
@@ -111,3 +153,72 @@ class QuantLinearInferOp:
     def backward(self, state, dy2d, need_weight_grad=True):
         from .tuning import dgrad_host
         return dgrad_host(self.q, dy2d), None
+
+
+def _np(a):
+    return a.cpu().numpy() if hasattr(a, "is_cuda") else np.asarray(a)
+
+
+def quantize_model(dense, hess, *, k: int = 8, bits: int = 4, g: int | None = 32, mode: str = "optq",
+                   reorder: str = "ogr", grid_steps: int = 100, alpha_min: float = 0.5,
+                   gwc=None, plan=None, meta: dict | None = None) -> QuantizedModel:
+    """Quantize every block linear of a dense model (qmodel.py:82-156), on the GPU.
+
+    `hess` is a calibration.HessianFull (per-layer 2 X X^T means in the ORIGINAL channel
+    order; CUDA tensors from accumulate_hessian_full, or host arrays), reindexed to follow each
+    layer's permutation. Reordering:
+      ogr     select_global -> build_plan -> apply_ogr; every layer structured except wo,
+              which stays irregular with its local weak set (qmodel.py:117-131);
+      online  per-layer local top-k moved to the tail, input_perm stored (qmodel.py:132-141);
+      none    per-layer local top-k, irregular layout (qmodel.py:142-147).
+    Every quantize_layer call runs the GPU quantizer (RTN, or alpha-grid + OPTQ with the
+    device fp64 factor). Passing gwc/plan reuses a previous selection."""
+    from .calibration import select_global, select_local_topk
+    from .errors import ConfigError
+    from .quantizer import LAYOUT_IRREGULAR, LAYOUT_STRUCTURED, quantize_layer
+    from .reorder import apply_ogr, build_plan, identity_plan, permute_hessian, weak_to_tail
+    cfg = dense.config
+    if reorder not in REORDER_MODES:
+        raise ConfigError(f"reorder must be one of {REORDER_MODES}")
+    lam = hess.diag()
+    if reorder == "ogr":
+        if gwc is None:
+            gwc = select_global(lam, k, n_blocks=cfg.n_blocks)
+        if plan is None:
+            plan = build_plan(gwc, cfg)
+        src = apply_ogr(dense, plan)
+    else:
+        gwc = None
+        plan = identity_plan(cfg)
+        src = dense.copy()
+    blocks = []
+    for i, b in enumerate(src.blocks):
+        layers = {}
+        for nm in BLOCK_LINEARS:
+            name = f"b{i}.{nm}"
+            w = _np(getattr(b, nm))
+            h = hess.h[name]
+            ge = g or w.shape[1] - k
+            common = dict(k=k, bits=bits, g=ge, mode=mode, grid_steps=grid_steps, alpha_min=alpha_min)
+            if reorder == "ogr":
+                if nm == "wo":
+                    layers[nm] = quantize_layer(w, layout=LAYOUT_IRREGULAR, indices=gwc.wo_indices[i], h=h,
+                                                **common)
+                else:
+                    perm = plan.p_ffn[i] if nm == "w_down" else plan.p_resid
+                    layers[nm] = quantize_layer(w, layout=LAYOUT_STRUCTURED, h=permute_hessian(h, perm),
+                                                **common)
+            elif reorder == "online":
+                perm = weak_to_tail(w.shape[1], select_local_topk(lam.lam[name], k))
+                q = quantize_layer(perm.apply_cols(w), layout=LAYOUT_STRUCTURED, h=permute_hessian(h, perm),
+                                   **common)
+                q.input_perm = perm.perm
+                layers[nm] = q
+            else:
+                layers[nm] = quantize_layer(w, layout=LAYOUT_IRREGULAR,
+                                            indices=select_local_topk(lam.lam[name], k), h=h, **common)
+        blocks.append(QuantBlock(gain1=_np(b.gain1).copy(), gain2=_np(b.gain2).copy(), layers=layers))
+    return QuantizedModel(config=cfg, embedding=_np(src.embedding).copy(), blocks=blocks,
+                          final_gain=_np(src.final_gain).copy(), head=_np(src.head).copy(), plan=plan,
+                          gwc=gwc, k=k, bits=bits, g=(g if g is not None else -1), mode=mode, reorder=reorder,
+                          fingerprint=model_fingerprint(cfg), meta=dict(meta or {}))

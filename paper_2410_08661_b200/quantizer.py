@@ -6,11 +6,14 @@ byte format (so it interchanges with the reference's containers and tests);
   * mode="rtn": min-max params + nearest codes in one CUDA kernel
     (libqeft_b200 `qeft_quantize_rtn`), bit-exact with quantizer.py:115-120,
     211-218;
-  * mode="optq": the alpha-grid parameter search (quantizer.py:144-179) and
-    the OPTQ column loop with inverse-Hessian error feedback
-    (quantizer.py:221-259), evaluated in fp64 on the GPU with torch linear
-    algebra (inv / cholesky). Codes match the reference except where the
-    BLAS/cuSOLVER rounding of H^-1 moves a value across a rounding boundary.
+  * mode="optq": the alpha-grid parameter search (quantizer.py:144-179, CUDA kernel,
+    bit-exact) and the OPTQ column loop with inverse-Hessian error feedback
+    (quantizer.py:221-259): H = 2 X X^T (fp64 GEMM on the GPU when X is given), the factor
+    U = chol(inv(H + damping))^T in fp64 on the GPU (cuSOLVER via torch.linalg; set
+    QEFT_OPTQ_FACTOR=host for the reference's own LAPACK factor), and the O(oc m^2) sweep in
+    the `qeft_optq_codes` kernel, bit-exact given the factor. Codes match the reference
+    except where the LAPACK vs cuSOLVER rounding of the factor moves a value across a
+    rounding boundary.
 Weak-column selection (irregular layouts) reuses calibration.select_local_topk
 and is bit-exact.
 """
@@ -167,16 +170,42 @@ def _optq_factor(h):
         return None
 
 
-def _optq_gpu(w_dense, h, sc, zr, g, bits):
-    """Greedy OPTQ rounding (quantizer.py:221-259): the O(oc*m^2) column sweep runs in
-    libqeft_b200 (`qeft_optq_codes`), bit-exact given the host factor."""
+def _optq_factor_device(h):
+    """The same factor in fp64 on the GPU (cuSOLVER getrf/getri + potrf through torch.linalg);
+    None where the reference would fall back (singular H or a non-positive-definite inverse)."""
     import torch
-    u = _optq_factor(h)
-    if u is None:
+    hd = h.to(torch.float64).clone()
+    damp = OPTQ_DAMP_FRAC * float(hd.diagonal().mean())
+    hd.diagonal().add_(damp)
+    hinv, info = torch.linalg.inv_ex(hd)
+    if int(info) != 0 or not bool(torch.isfinite(hinv).all()):
+        return None
+    lo, info = torch.linalg.cholesky_ex(hinv)
+    if int(info) != 0:
+        return None
+    return lo.T.contiguous()
+
+
+def optq_factor_mode() -> str:
+    import os
+    return os.environ.get("QEFT_OPTQ_FACTOR", "device")
+
+
+def _optq_gpu(w_dense, h, sc, zr, g, bits):
+    """Greedy OPTQ rounding (quantizer.py:221-259): factor on the GPU (or the host LAPACK one,
+    QEFT_OPTQ_FACTOR=host), then the O(oc*m^2) column sweep in libqeft_b200 (`qeft_optq_codes`),
+    bit-exact given the factor."""
+    import torch
+    if optq_factor_mode() == "host":
+        u = _optq_factor(h.cpu().numpy() if hasattr(h, "is_cuda") else h)
+        ud = None if u is None else torch.from_numpy(u).cuda()
+    else:
+        hd = h if hasattr(h, "is_cuda") else torch.from_numpy(np.ascontiguousarray(h, np.float64)).cuda()
+        ud = _optq_factor_device(hd)
+    if ud is None:
         return None
     oc, m = w_dense.shape
     w = torch.from_numpy(np.array(w_dense, np.float64)).cuda()
-    ud = torch.from_numpy(u).cuda()
     s = torch.from_numpy(np.ascontiguousarray(sc, np.float32)).cuda()
     z = torch.from_numpy(np.ascontiguousarray(zr, np.float32)).cuda()
     err = torch.empty((oc, m), dtype=torch.float64, device="cuda")
@@ -226,16 +255,21 @@ def quantize_layer(w, *, k: int, bits: int, g: int, mode: str = "optq",
     else:
         scales, zeros = _grid_params_gpu(w_dense, g_eff, bits, grid_steps, alpha_min)
         if m > 0:
+            import torch
             if h is None:
                 if x is None:
                     raise ShapeError("optq mode needs calibration x or h")
-                xs = np.asarray(x, dtype=np.float64)
+                xs = (x if hasattr(x, "is_cuda") else torch.from_numpy(np.asarray(x, np.float64))).cuda().double()
                 if xs.shape[0] != ic:
                     raise ShapeError(f"calibration rows {xs.shape[0]} != IC {ic}")
-                h = 2.0 * xs @ xs.T
-            hq = np.asarray(h, dtype=np.float64)[np.ix_(qpos, qpos)]
-            if hq.shape != (m, m):
-                raise ShapeError(f"Hessian {hq.shape} does not match {m} columns")
+                h = torch.matmul(xs, xs.T).mul_(2.0)  # quantizer.py:324-332, fp64 GEMM on the GPU
+            if hasattr(h, "is_cuda"):
+                qi = torch.from_numpy(qpos).to(h.device)
+                hq = h.double().index_select(0, qi).index_select(1, qi)
+            else:
+                hq = np.asarray(h, dtype=np.float64)[np.ix_(qpos, qpos)]
+            if tuple(hq.shape) != (m, m):
+                raise ShapeError(f"Hessian {tuple(hq.shape)} does not match {m} columns")
             codes = _optq_gpu(w_dense, hq, scales, zeros, g_eff, bits)
             if codes is None:
                 codes, fallback = _nearest_codes_gpu(w_dense, scales, zeros, g_eff, bits), True

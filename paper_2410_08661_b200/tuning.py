@@ -175,28 +175,40 @@ def sample_windows(rng, ids, n, seq_len):
 
 
 def rank_micro_batches(rng, ids, cfg: TuneConfig, rank: int = 0, world: int = 1):
-    """One optimizer step's micro-batches for `rank` of `world`.
+    """One optimizer step's work for `rank` of `world`: [(index, inputs, targets, weight)].
 
-    Every rank draws the full stream of `grad_accum` windows from the shared
-    generator, in the reference's order (tuning.py:209-213), and keeps those with
-    index % world == rank, so the union over ranks is exactly the reference's
-    accumulation group and the generator stays in lockstep across ranks.
-    Returns [(index, inputs, targets), ...].
+    Every rank draws the full stream of `grad_accum` micro-batches of `batch` windows from the
+    shared generator, in the reference's order (tuning.py:209-213), so the generator stays in
+    lockstep and the union over ranks is exactly the reference's accumulation group.
+      world <= grad_accum: rank r takes whole micro-batches i with i % world == r (weight 1);
+      world  > grad_accum: the grad_accum * batch windows are dealt round-robin (window w to
+                           rank w % world) so no rank idles; a rank's windows are cut into
+                           chunks of <= batch windows, each weighted n_windows / batch.
+    The caller backpropagates weight * mean-loss(chunk) and divides the summed gradients by
+    grad_accum, which reproduces the reference's sum-of-micro-batch-means / grad_accum
+    (tuning.py:219-228) for every world size (exactly when the weights are powers of two).
     """
+    draws = [sample_windows(rng, ids, cfg.batch, cfg.seq_len) for _ in range(cfg.grad_accum)]
+    if world <= cfg.grad_accum:
+        return [(i, xb, yb, 1.0) for i, (xb, yb) in enumerate(draws) if i % world == rank]
+    xs = np.concatenate([d[0] for d in draws])
+    ys = np.concatenate([d[1] for d in draws])
+    mine = np.arange(rank, xs.shape[0], world)
     out = []
-    for i in range(cfg.grad_accum):
-        xb, yb = sample_windows(rng, ids, cfg.batch, cfg.seq_len)
-        if i % world == rank:
-            out.append((i, xb, yb))
+    for c in range(0, mine.size, cfg.batch):
+        idx = mine[c:c + cfg.batch]
+        out.append((c // cfg.batch, xs[idx], ys[idx], idx.size / cfg.batch))
     return out
 
 
 def dp_allreduce_(grad, loss_sum, group=None):
-    """Sum the flat weak-gradient bucket and the loss sum over the DP group
-    (one collective each; a no-op for a single process)."""
+    """Sum the flat weak-gradient bucket (None: already reduced bucket by bucket during the
+    backward, WeakTrainer.arm_overlap) and the loss sum over the DP group; a no-op for a single
+    process."""
     import torch.distributed as dist
     if group is not None and dist.get_world_size(group) > 1:
-        dist.all_reduce(grad, group=group)
+        if grad is not None:
+            dist.all_reduce(grad, group=group)
         dist.all_reduce(loss_sum, group=group)
     return grad, loss_sum
 
@@ -231,9 +243,64 @@ class WeakTrainer:
             l.weak32.grad = self.grad[off:off + sz].view(l.oc, l.k)
         self.descs, self.max_elems = optim.shadow_descs([l.dl for l in self.lins],
                                                         [int(o) for o in self.offsets[:-1]])
+        self.max_rows = max((l.oc for l in self.lins), default=0)
         self.step_no = 0
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
         self.sq = torch.zeros(1, dtype=torch.float64, device=dev)
+        # per-block buckets for the overlapped all-reduce: a contiguous slice of
+        # the flat bucket per decoder block, launched as soon as the block's last dW lands
+        blk = [l.name.split(".")[0] if "." in l.name else str(i) for i, l in enumerate(self.lins)]
+        self.bucket_of, self.bucket_range, self.bucket_size = [], [], []
+        for i, b in enumerate(blk):
+            if not self.bucket_range or blk[i - 1] != b:
+                self.bucket_range.append([int(self.offsets[i]), int(self.offsets[i + 1])])
+                self.bucket_size.append(0)
+            self.bucket_range[-1][1] = int(self.offsets[i + 1])
+            self.bucket_size[-1] += 1
+            self.bucket_of.append(len(self.bucket_range) - 1)
+        self._pending = None
+        self._works = []
+        for i, l in enumerate(self.lins):
+            l.grad_ready_hook = (lambda mod, i=i: self._grad_ready(i))
+
+    def arm_overlap(self):
+        """The next backward is the step's last on this rank: all-reduce every block's bucket
+        on the collective's own stream as soon as all of its layers' dW_weak are in."""
+        import torch.distributed as dist
+        if self.group is None or dist.get_world_size(self.group) <= 1:
+            return
+        self._pending = list(self.bucket_size)
+
+    def _grad_ready(self, i):
+        if self._pending is None:
+            return
+        b = self.bucket_of[i]
+        self._pending[b] -= 1
+        if self._pending[b] == 0:
+            self._launch(b)
+
+    def _launch(self, b):
+        import torch.distributed as dist
+        lo, hi = self.bucket_range[b]
+        self._works.append(dist.all_reduce(self.grad[lo:hi], group=self.group, async_op=True))
+        self._pending[b] = -1
+
+    def flush_overlap(self):
+        """Launch the buckets that did not fire (layers without a weak block or no backward)."""
+        if self._pending is None:
+            return
+        for b, c in enumerate(self._pending):
+            if c >= 0:
+                self._launch(b)
+
+    def wait_allreduce(self):
+        """Make the current stream wait for the launched bucket all-reduces."""
+        if self._pending is not None:
+            self.flush_overlap()
+        for w in self._works:
+            w.wait()
+        self._works = []
+        self._pending = None
 
     @property
     def n_params(self) -> int:
@@ -244,7 +311,9 @@ class WeakTrainer:
 
     def step(self, n_micro_total: int, loss_sum=None, reduced: bool = False):
         """All-reduce (DP, unless `reduced`) -> /(grad_accum * loss_scale) -> clip -> Adam
-        -> weak16 refresh. Returns the pre-clip global gradient norm (device fp64)."""
+        -> weak16 refresh, in two passes over the bucket (libqeft_b200 qeft_grad_sqnorm_div +
+        qeft_adam_step_flat; the divide is folded into both, the grads are left untouched).
+        Returns the pre-clip global gradient norm squared (device fp64)."""
         import torch
         from . import optim
         cfg = self.cfg
@@ -252,16 +321,15 @@ class WeakTrainer:
             if loss_sum is None:
                 loss_sum = torch.zeros((), dtype=torch.float64, device=self.grad.device)
             dp_allreduce_(self.grad, loss_sum, self.group)
-        optim.div_(self.grad, float(n_micro_total) * self.loss_scale)
-        optim.grad_sqnorm(self.grad, out=self.sq)
+        self.wait_allreduce()
+        div = float(n_micro_total) * self.loss_scale  # loss_scale is a power of two: exact
+        optim.grad_sqnorm_div(self.grad, div, out=self.sq)
         self.step_no += 1
         self.flag.zero_()
-        optim.adam_clip_(self.w32, self.m, self.v, self.grad, self.step_no, cfg.lr,
-                         max_norm=cfg.max_grad_norm, beta1=cfg.beta1, beta2=cfg.beta2, eps=cfg.eps,
-                         sqnorm=self.sq, flag=self.flag)
-        optim.refresh_shadows(self.w32, self.descs, len(self.lins), self.max_elems)
+        optim.adam_step_flat(self.w32, self.m, self.v, self.grad, self.descs, len(self.lins), self.max_rows, div,
+                             self.step_no, cfg.lr, max_norm=cfg.max_grad_norm, sqnorm=self.sq, flag=self.flag,
+                             beta1=cfg.beta1, beta2=cfg.beta2, eps=cfg.eps)
         return self.sq
-
 
 def _ddp_group():
     import torch.distributed as dist
@@ -309,13 +377,19 @@ def finetune(qm, dataset, config: TuneConfig | None = None, *, act_dtype: str = 
     for step in range(1, cfg.steps + 1):
         tr.zero_grad()
         loss_sum = torch.zeros((), dtype=torch.float64, device=dev)
-        for _, xb, yb in rank_micro_batches(rng, ids, cfg, rank, world):
+        work = rank_micro_batches(rng, ids, cfg, rank, world)
+        for ci, (_, xb, yb, wgt) in enumerate(work):
+            if ci == len(work) - 1:
+                tr.arm_overlap()  # the last backward all-reduces each block's bucket as it lands
             xt = torch.from_numpy(np.asarray(xb, np.int64)).to(dev)
             yt = torch.from_numpy(np.asarray(yb, np.int64)).to(dev)
             loss = cross_entropy_mean(model(xt), yt)
-            (loss * loss_scale).backward()
-            loss_sum += loss.detach().double()
-        dp_allreduce_(tr.grad, loss_sum, group)
+            (loss * (loss_scale * wgt)).backward()
+            loss_sum += loss.detach().double() * wgt
+        if not work:  # nothing to backprop on this rank: its (zero) bucket still joins the sum
+            tr.arm_overlap()
+            tr.flush_overlap()
+        dp_allreduce_(None, loss_sum, group)
         loss_mean = float(loss_sum) / cfg.grad_accum
         if not math.isfinite(loss_mean):
             # the masters still hold the last finite update (tuning.py:215-218)

@@ -318,10 +318,65 @@ def gen_container():
     np.savez_compressed(os.path.join(OUT, "container.npz"), **d)
 
 
+def gen_qmodel():
+    """Whole-model quantization (qmodel.py:82-156) on the toy model of gen_finetune: the dense
+    weights, the traced calibration activations of every window (what collect_calibration feeds
+    accumulate_hessian_full, calibration.py:113-122, 234-244), the reference's full Hessians,
+    its global weak-column selection and OGR plan, and the quantized models for reorder modes
+    ogr / online / none (RTN, so codes are BLAS-independent)."""
+    from qeft import model as M
+    from qeft import qmodel as Q
+    cfg = M.ModelConfig(d_model=32, n_heads=4, head_dim=8, d_ff=64, n_blocks=2,
+                        vocab_size=256, max_seq=64, seed=5)
+    dense = M.init_model(cfg)
+    ids = np.random.default_rng(77).integers(0, 256, size=4000).astype(np.int64)
+    d = {"cfg": np.array([cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.d_ff, cfg.n_blocks,
+                          cfg.vocab_size, cfg.max_seq, cfg.seed])}
+    d["embedding"], d["head"], d["final_gain"] = dense.embedding, dense.head, dense.final_gain
+    for i, b in enumerate(dense.blocks):
+        for f in ("gain1", "gain2", "wq", "wk", "wv", "wo", "w_up", "w_gate", "w_down"):
+            d[f"b{i}_{f}"] = getattr(b, f)
+    # calibration_windows + traced forwards, exactly as collect_calibration does
+    em = M.dense_engine(dense) if hasattr(M, "dense_engine") else calibration.dense_engine(dense)
+    windows = calibration.calibration_windows(ids, 4, min(48, cfg.max_seq), 0)
+    names = None
+    for w, row in enumerate(windows):
+        _, trace, _ = M.forward_batch(em, row[None, :], want_trace=True)
+        names = list(trace.activations)
+        for nm, x in trace.activations.items():
+            d[f"act{w}_{nm}"] = x
+    d["n_windows"] = len(windows)
+    d["layer_names"] = np.array(names)
+    hess = calibration.collect_calibration(dense, ids, n_seq=4, seq_len=48, seed=0)
+    for nm, h in hess.h.items():
+        d["h_" + nm] = h
+    for reo in ("ogr", "online", "none"):
+        qm = Q.quantize_model(dense, hess, k=4, bits=4, g=16, mode="rtn", reorder=reo)
+        pre = reo + "_"
+        d[pre + "embedding"], d[pre + "head"], d[pre + "final_gain"] = qm.embedding, qm.head, qm.final_gain
+        for i, b in enumerate(qm.blocks):
+            d[pre + f"b{i}_gain1"], d[pre + f"b{i}_gain2"] = b.gain1, b.gain2
+        for name, q in qm.layer_items():
+            _layer_dict(pre + name + "_", q, d)
+            d[pre + name + "_input_perm"] = (q.input_perm if q.input_perm is not None
+                                            else np.zeros(0, np.int64))
+        if reo == "ogr":
+            d["gwc_resid"] = qm.gwc.resid_indices
+            d["gwc_s_global"] = qm.gwc.s_global
+            for i in range(cfg.n_blocks):
+                d[f"gwc_ffn{i}"] = qm.gwc.ffn_indices[i]
+                d[f"gwc_wo{i}"] = qm.gwc.wo_indices[i]
+                d[f"plan_ffn{i}"] = qm.plan.p_ffn[i].perm
+            d["plan_resid"] = qm.plan.p_resid.perm
+            d["fingerprint"] = np.array(qm.fingerprint)
+    np.savez_compressed(os.path.join(OUT, "qmodel.npz"), **d)
+
+
 if __name__ == "__main__":
     # `make_golden.py [packing quantizer training selection finetune]` (default: all)
     gens = {"packing": gen_packing, "quantizer": gen_quantizer, "training": gen_training,
-            "selection": gen_selection, "finetune": gen_finetune, "container": gen_container}
+            "selection": gen_selection, "finetune": gen_finetune, "container": gen_container,
+            "qmodel": gen_qmodel}
     for name in (sys.argv[1:] or list(gens)):
         gens[name]()
     for f in sorted(os.listdir(OUT)):
