@@ -138,7 +138,8 @@ def cpu_oracle_sample(seconds: float = 10.0, seed: int = 0):
                                     zeros=zr, weak=weak, weak_indices=np.arange(m, ic),
                                     layout="structured"))
     xs = {ic: rng.standard_normal(ic).astype(np.float32) for _, ic in BLOCK_SHAPES}
-    nbytes = [O.row_bytes(q.m, 4) * q.oc + 8 * q.oc * q.n_groups + 2 * q.oc * q.k
+    # the same SURVEY 8(d) bytes as the GPU line (codes + 4 B per row and group + fp16 weak + x, y)
+    nbytes = [O.row_bytes(q.m, 4) * q.oc + 4 * q.oc * q.n_groups + 2 * q.oc * q.k
               + 2 * (q.ic + q.oc) for q in layers]
     O.matvec_structured(layers[0], xs[layers[0].ic])  # warm
     done_b, calls, t0 = 0, 0, time.perf_counter()
@@ -156,6 +157,46 @@ def cpu_oracle_sample(seconds: float = 10.0, seed: int = 0):
     except Exception:
         cores = os.cpu_count()
     return done_b / dt / 1e9, f"{calls} matvec_structured calls over one 7B decoder block (7 layers), {dt:.1f} s", cores
+
+
+def finetune_cpu_baseline(seconds: float = 12.0, T: int = 256):
+    """CPU reference of the fine-tune step's linears: the oracle port of
+    qlinear_forward_train + qlinear_backward (tuning.py:52-103; per-call dense dequant, BLAS
+    fp32 GEMMs) on one layer of each 7B shape at T tokens, timed until `seconds` elapse, and
+    EXTRAPOLATED to the 32-block step (per-token cost x 7 layers x 32 blocks). Attention, norms
+    and the head are not included (they are not on the reference's quantized path)."""
+    from oracle import qeft_oracle as O
+    rng = np.random.default_rng(5)
+    per_tok = {}
+    t_end = time.perf_counter() + seconds
+    for oc, ic in ((4096, 4096), (11008, 4096), (4096, 11008)):
+        k, g, m = 128, 128, ic - 128
+        q = O.OracleLayer(oc=oc, ic=ic, k=k, bits=4, g=g,
+                          packed=rng.integers(0, 256, size=oc * O.row_bytes(m, 4), dtype=np.uint8).tobytes(),
+                          scales=(1e-3 + 0.01 * np.abs(rng.standard_normal((oc, O.n_groups(m, g))))).astype(np.float32),
+                          zeros=(0.05 * rng.standard_normal((oc, O.n_groups(m, g)))).astype(np.float32),
+                          weak=(0.02 * rng.standard_normal((oc, k))).astype(np.float32),
+                          weak_indices=np.arange(m, ic), layout="structured")
+        x = rng.standard_normal((ic, T)).astype(np.float32)
+        dy = rng.standard_normal((oc, T)).astype(np.float32)
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            _, xw = O.forward_train(q, x)
+            O.backward(q, xw, dy)
+            reps += 1
+            if time.perf_counter() >= min(t_end, t0 + seconds / 3):
+                break
+        per_tok[(oc, ic)] = (time.perf_counter() - t0) / reps / T
+    step_tok = 32 * sum(per_tok[(oc, ic)] for oc, ic in BLOCK_SHAPES)
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    return {"value": 1.0 / step_tok, "unit": "tokens/s", "cores": cores, "kind": "port",
+            "extrapolated": True,
+            "sample": "oracle qlinear_forward_train + qlinear_backward, one layer of each 7B shape at "
+                      f"T={T}, {seconds:.0f} s; x 7 layers x 32 blocks (linears only)"}
 
 
 def run_reference(args):
@@ -221,6 +262,58 @@ def kernel_roofline(torch, n_blocks, peak, n_cols, fuse=True):
         out.append({"launch": name, "shapes": [list(x) for x in shapes], "us_per_launch": per_launch * 1e6,
                     "bytes_per_launch": nb, "achieved_gbs": nb / per_launch / 1e9,
                     "frac": nb / per_launch / 1e9 / peak})
+        del st, layers
+    return out
+
+
+def layout_bench(torch, peak):
+    """The reference's three layouts on the 4096 x 4096 shape (OGR models keep W_O irregular,
+    qmodel.py:117-131; online reordering gives every layer an input_perm, 132-141): the decode
+    GEMV (N=1, 32 distinct layers per graph: HBM-resident) and the prefill/fine-tune GEMMs at
+    T=2048. Structured layers read x in place; irregular / online ones gather x through the
+    column map (in the GEMV's x staging; a gather pre-pass in the GEMM) and scatter dX."""
+    from paper_2410_08661_b200.decode import LinearStack, random_layer
+    from paper_2410_08661_b200.layer import DeviceLayer
+    rng = np.random.default_rng(7)
+    ic, k = 4096, 128
+
+    def variant(dl, kind):
+        if kind == "structured":
+            return dl
+        if kind == "irregular":
+            weak = np.sort(rng.choice(ic, k, replace=False))
+            keep = np.setdiff1d(np.arange(ic), weak)
+            perm = np.concatenate([keep, weak])
+        else:
+            perm = rng.permutation(ic)
+        colmap = np.full(dl.m_pad + dl.k_pad, -1, np.int32)
+        colmap[:dl.m] = perm[:dl.m]
+        colmap[dl.m_pad:dl.m_pad + k] = perm[dl.m:]
+        return DeviceLayer(oc=dl.oc, ic=dl.ic, k=dl.k, bits=dl.bits, g=dl.g, qweight=dl.qweight, sz=dl.sz,
+                           weak16=dl.weak16, colmap=torch.from_numpy(colmap).cuda(), dtype=dl.dtype,
+                           weak32=dl.weak32, sz16=dl.sz16)
+
+    out = []
+    bpk = _bf16_peak(burst=True)
+    for kind in ("structured", "irregular", "online"):
+        layers = [variant(random_layer(4096, ic, k, 4, 128, "f16", seed=500 + i), kind) for i in range(32)]
+        st = LinearStack(layers, n_cols=1)
+        for _ in range(3):
+            st.step()
+        t = _time_graph(st.step, 20, torch) / (20 * 32)
+        nb = st.bytes_per_step() / 32
+        x = torch.randn(2048, ic, device="cuda", dtype=torch.float16)
+        dy = torch.randn(2048, 4096, device="cuda", dtype=torch.float16)
+        L0 = layers[0]
+        for _ in range(3):
+            L0.gemm_fwd(x)
+            L0.gemm_dgrad(dy)
+        tf = _time_graph(lambda: L0.gemm_fwd(x), 20, torch) / 20
+        td = _time_graph(lambda: L0.gemm_dgrad(dy), 20, torch) / 20
+        fl = 2.0 * 2048 * 4096 * ic
+        out.append({"layout": kind, "gemv_us": t * 1e6, "gemv_gbs": nb / t / 1e9, "gemv_frac": nb / t / 1e9 / peak,
+                    "gemm_fwd_tflops": fl / tf / 1e12, "gemm_dgrad_tflops": fl / td / 1e12,
+                    "gemm_fwd_frac": fl / tf / 1e12 / bpk, "gemm_dgrad_frac": fl / td / 1e12 / bpk})
         del st, layers
     return out
 
@@ -319,6 +412,7 @@ def run_b200(args):
     n_layers = len(layers)
     del stack, layers
     torch.cuda.empty_cache()
+    lay = layout_bench(torch, peak) if (rank == 0 and not args.no_sweep) else None
     ds = None if (args.no_dstep or rank != 0) else decode_step_bench(args, torch, dev)
     torch.cuda.empty_cache()
     ft = None if args.no_ft else finetune_bench(args, ws, rank, dev, torch)
@@ -359,7 +453,10 @@ def run_b200(args):
             "finetune": ft,
             "decode_step": ds,
             "batch_sweep": sweep or None,
+            "layouts": lay,
         }
+        if ft is not None and ws == 1 and not args.no_cpu:
+            ft["cpu_baseline"] = finetune_cpu_baseline()
         line["e2e"]["h2d_bytes_per_step"] = sum(2 * n * ic for ic in sorted({s[1] for s in BLOCK_SHAPES}))
         line["e2e"]["d2h_bytes_per_step"] = sum(2 * n * oc for oc, _ in BLOCK_SHAPES) * args.blocks
         print(json.dumps(line), flush=True)

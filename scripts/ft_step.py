@@ -15,7 +15,7 @@ ap.add_argument("--steps", type=int, default=5)
 args = ap.parse_args()
 cfg = ModelConfig(**{**LLAMA2_7B.__dict__, "n_blocks": args.blocks})
 t0 = time.time()
-model = QEFTDecoder.synthetic(cfg, k=128, bits=4, g=128, act_dtype="bf16", compute_dtype="bf16")
+model = QEFTDecoder.synthetic(cfg, k=128, bits=4, g=128, act_dtype="f16", compute_dtype="f16")
 tr = WeakTrainer(model, TuneConfig(lr=5e-6, max_grad_norm=0.3))
 torch.cuda.synchronize()
 print("build s", round(time.time() - t0, 1), "weak params", tr.n_params, "mem GB", round(torch.cuda.memory_allocated() / 1e9, 2), flush=True)

@@ -5,16 +5,17 @@
 set -x
 O=gpurun_out/evidence
 mkdir -p $O
-timeout 900 python -m pytest tests -m gpu -q > $O/pytest_gpu.txt 2>&1; tail -2 $O/pytest_gpu.txt
+timeout 1200 python -m pytest tests -m gpu -q > $O/pytest_gpu.txt 2>&1; tail -2 $O/pytest_gpu.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1; tail -2 $O/smoke.txt
-timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
+timeout 1200 python bench.py > $O/bench.json 2> $O/bench.err
+timeout 600 python scripts/configs_perf.py > $O/configs_perf.json 2> $O/configs_perf.err
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
-timeout 600 ncu --metrics $M --clock-control none -k regex:gemv_kernel -c 256 --csv --log-file $O/decode_launches.csv \
+timeout 600 ncu --metrics $M --clock-control none -k regex:gemv -c 256 --csv --log-file $O/decode_launches.csv \
   python bench.py --steps 1 --warmup 3 --no-ft --no-dstep --no-sweep --no-cpu > /dev/null 2>&1
 timeout 900 ncu --metrics $M --clock-control none --csv --log-file $O/ft_launches.csv \
   python scripts/ft_step.py --blocks 2 --steps 1 > /dev/null 2>&1
 for t in qkv o gate_up down; do
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv_kernel -s 2 -c 1 -o /tmp/gemv_$t \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv2_kernel -s 2 -c 1 -o /tmp/gemv_$t \
     python scripts/prof_decode.py $t > /dev/null 2>&1
   ncu -i /tmp/gemv_$t.ncu-rep --page raw --csv > $O/gemv_${t}_raw.csv
   ncu -i /tmp/gemv_$t.ncu-rep --page source --csv > $O/gemv_${t}_source.csv
