@@ -5,8 +5,9 @@ own column order (quantizer.py:95-100); backward gives dX through the full
 W_hat and dW only for the weak block, computed from the saved weak slice of
 the input (the reference's qlinear_forward_train / qlinear_backward,
 pkg/src/qeft/tuning.py:52-103). Every product runs in libqeft_b200:
-  T <= 16 tokens  -> decode GEMV (qeft_gemv)
-  T  > 16 tokens  -> tcgen05 GEMM (qeft_gemm_fwd)
+  inference, T <= 16 tokens -> decode GEMV (qeft_gemv)
+  otherwise                 -> tcgen05 GEMM (qeft_gemm_fwd); training always takes the GEMM,
+                               whose dequantized weights are exactly the dX GEMM's
   backward        -> qeft_gemm_dgrad + qeft_gemm_wgrad_weak
 The fp32 master of the weak block is the module's only Parameter; its .grad is
 a view into the owner's flat gradient bucket when one is attached (the DP step
@@ -25,13 +26,9 @@ from .layer import DeviceLayer, _DT
 
 class _QEFTLinearFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x2, weak32, mod):
+    def forward(ctx, x2, weak32, mod, use_gemv):
         dl: DeviceLayer = mod.dl
-        T = x2.shape[0]
-        if T <= 16:
-            y = dl.gemv(x2)
-        else:
-            y = dl.gemm_fwd(x2)
+        y = dl.gemv(x2) if use_gemv else dl.gemm_fwd(x2)
         ctx.mod = mod
         if weak32.requires_grad and dl.k:
             ctx.save_for_backward(dl.gather_weak(x2))
@@ -57,7 +54,7 @@ class _QEFTLinearFn(torch.autograd.Function):
             dl.gemm_wgrad_weak(dy, xw, out=w.grad, accumulate=True)
             if mod.grad_ready_hook is not None:  # e.g. launch this layer group's DP all-reduce
                 mod.grad_ready_hook(mod)
-        return dx, None, None
+        return dx, None, None, None
 
 
 class QEFTLinear(torch.nn.Module):
@@ -89,7 +86,10 @@ class QEFTLinear(torch.nn.Module):
         x2 = x.reshape(-1, self.ic)
         if x2.dtype != self.dl.tdtype:
             x2 = x2.to(self.dl.tdtype)
-        y = _QEFTLinearFn.apply(x2, self.weak32, self)
+        # inference on <= 16 tokens: the decode GEMV; training: the GEMM (the dX GEMM's weights)
+        use_gemv = x2.shape[0] <= 16 and not (torch.is_grad_enabled() and
+                                              (self.weak32.requires_grad or x2.requires_grad))
+        y = _QEFTLinearFn.apply(x2, self.weak32, self, use_gemv)
         return y.reshape(*lead, self.oc)
 
     @torch.no_grad()

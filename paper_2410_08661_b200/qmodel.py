@@ -134,7 +134,9 @@ class QuantLinearInferOp:
     quant_engine / quantized_perplexity (qmodel.py:206-224). The reference dequantizes once
     and multiplies dense fp32; here the layer is repacked once into the B200 layout
     (layer.device_layer) and every call runs the fused kernels: the decode GEMV for <= 16
-    activation columns, the tcgen05 GEMM above. backward returns (dX, None): no weight grad."""
+    activation columns, the tcgen05 GEMM above. backward returns (dX, None): no weight grad.
+    The kernel path reads x in the layer's input order; an online layer's colmap applies
+    input_perm (as qlinear_forward_train does, tuning.py:64-65)."""
 
     def __init__(self, name: str, q):
         from .layer import device_layer
@@ -144,6 +146,11 @@ class QuantLinearInferOp:
         device_layer(q, "f16")  # build the device copy now (the reference's dequant-once)
 
     def apply(self, x2d):
+        """<= 16 columns: the decode GEMV (one pass over the packed weights); more: the GEMM."""
+        x2d = np.asarray(x2d, np.float32)
+        if x2d.shape[1] <= 16:
+            from .kernels import _run
+            return _run(self.q, x2d, perm=None)
         from .tuning import qlinear_forward_train
         return qlinear_forward_train(self.q, x2d)[0]
 

@@ -68,7 +68,8 @@ def _to_dev(a: np.ndarray, scale: float):
 
 
 def qlinear_forward_train(q, x, *, w_hat_dense=None):
-    """Y = W_hat_full @ X, saving only X[weak] (tuning.py:52-72). x: (IC, T) f32."""
+    """Y = W_hat_full @ X, saving only X[weak] (tuning.py:52-72). x: (IC, T) f32; the product
+    runs in the tcgen05 forward GEMM (fp16 operands, fp32 accumulation)."""
     x = np.asarray(x, dtype=np.float32)
     if x.ndim != 2 or x.shape[0] != q.ic:
         raise ShapeError(f"input rows {x.shape[0] if x.ndim else 0} != IC {q.ic}")
@@ -80,7 +81,10 @@ def qlinear_forward_train(q, x, *, w_hat_dense=None):
     dl = device_layer(q, "f16")
     s = _pow2_scale(x)
     xt = _to_dev(x, s)
-    y = dl.gemm_fwd(xt) if T > 16 else dl.gemv(xt, out_f32=True)
+    # the tcgen05 GEMM at every T: the same dequantized weights as the backward's dX GEMM, so
+    # the gradients are those of this forward (the decode GEMV's fp16 (scale, zero) pairs serve
+    # inference only: QuantLinearInferOp, KernelPathOp, the decode stack)
+    y = dl.gemm_fwd(xt)
     return (y.float().cpu().numpy().T / np.float32(s)).astype(np.float32), state
 
 
