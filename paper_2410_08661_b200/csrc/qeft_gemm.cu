@@ -20,6 +20,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 
 #include "qeft_common.cuh"
 #include "qeft_internal.h"
@@ -39,6 +41,7 @@ constexpr int kEpiWarps = 4;
 constexpr int kThreads = (2 + kProdWarps + kEpiWarps) * 32;  // TMA, MMA, producers, epilogue
 constexpr int kStageA = BM * BK * 2;    // 16 KB
 constexpr int kEpiStride = 40;          // halves per staging row (32 + 8 pad)
+constexpr int kRing = 8;                // stream-K fix-up: 4 KB bulk-copy slots per epilogue warp
 
 struct GemmArgs {
   const uint8_t* qw;
@@ -56,6 +59,73 @@ struct GemmArgs {
   int fast_out;   // dgrad: output columns contiguous in 32-blocks (structured, m % 32 == 0)
   int out_cols;   // fwd: oc; dgrad: ic
   int g_shift;    // log2(g) when g is a power of two, else -1 (group index without a divide)
+  // stream-K schedule (sk != 0): the n_items x n_kblk k-block units are cut into gridDim.x
+  // contiguous ranges; a tile split across CTAs is finished by the CTA holding its last k-block,
+  // which adds the fp32 partials the other CTAs left in part[cta] (flags[cta] = 1 when ready)
+  int sk;
+  float* part;
+  int* flags;
+};
+
+// The work of one CTA as a list of segments (tile, k-blocks [kb0, kb1)). Round-robin whole
+// tiles, or (stream-K) the tiles of the CTA's unit range ordered so that the one segment that
+// does NOT end its tile (a partial for a later CTA) runs first and the segment that finishes a
+// tile started by earlier CTAs runs last: producers publish early, finishers consume late, and a
+// CTA only ever waits on lower-numbered CTAs (no deadlock with in-order CTA dispatch).
+struct Seg {
+  int tile, kb0, kb1, fin;
+};
+struct SegPlan {
+  int nseg, b, G, nk, sk;
+  int t_first, head, tail, nfull;
+  int64_t u0, u1, U;
+  QEFT_DEV static int64_t ustart(int64_t p, int64_t U, int G) { return p * U / G; }
+  QEFT_DEV void init(int ntiles, int nk_, int sk_) {
+    b = blockIdx.x; G = gridDim.x; nk = nk_; sk = sk_;
+    if (!sk) {
+      nseg = ntiles > b ? (ntiles - 1 - b) / G + 1 : 0;
+      return;
+    }
+    U = (int64_t)ntiles * nk;
+    u0 = ustart(b, U, G);
+    u1 = ustart(b + 1, U, G);
+    if (u1 <= u0) {
+      nseg = 0;
+      return;
+    }
+    t_first = (int)(u0 / nk);
+    const int t_last = (int)((u1 - 1) / nk);
+    head = (u1 % nk) != 0;                                 // t_last's segment stops short of its end
+    tail = (u0 % nk) != 0 && !(t_first == t_last && head);  // t_first's segment finishes a split tile
+    nseg = t_last - t_first + 1;
+    nfull = nseg - head - tail;
+  }
+  QEFT_DEV Seg get(int i) const {
+    Seg s;
+    if (!sk) {
+      s.tile = b + i * G; s.kb0 = 0; s.kb1 = nk; s.fin = 1;
+      return s;
+    }
+    if (head && i == 0) {
+      const int t = (int)((u1 - 1) / nk);
+      s.tile = t;
+      s.kb0 = (int)(max(u0, (int64_t)t * nk) - (int64_t)t * nk);
+      s.kb1 = (int)(u1 - (int64_t)t * nk);
+      s.fin = 0;
+      return s;
+    }
+    const int j = i - head;
+    if (j < nfull) {
+      s.tile = t_first + tail + j; s.kb0 = 0; s.kb1 = nk; s.fin = 1;
+      return s;
+    }
+    s.tile = t_first;
+    s.kb0 = (int)(u0 - (int64_t)t_first * nk);
+    s.kb1 = nk;
+    s.fin = 1;
+    return s;
+  }
+  QEFT_DEV int64_t start_of(int p) const { return ustart(p, U, G); }
 };
 
 template <typename T>
@@ -204,10 +274,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
   T* sE = reinterpret_cast<T*>(sB + kStagesB * kStageB);  // epilogue staging [4 warps][32][kEpiStride]
   __shared__ __align__(8) uint64_t fullA[kStagesA], emptyA[kStagesA], fullB[kStagesB], emptyB[kStagesB];
   __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ __align__(8) uint64_t ring_full[kEpiWarps][kRing];  // stream-K fix-up ring
   __shared__ uint32_t tmem_base;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = a.n_items;
+  SegPlan plan;
+  plan.init(ntiles, a.n_kblk, a.sk);
   // work item -> (m-block, first token, sub-tiles). Items past n_full are the halves of the
   // last partial wave's tiles, so that wave spreads over twice as many SMs.
   struct Item {
@@ -241,6 +314,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       mbar_init(&tfull_bar[i], 1);
       mbar_init(&tempty_bar[i], kEpiWarps);
     }
+    for (int i = 0; i < kEpiWarps * kRing; ++i) mbar_init(&ring_full[i / kRing][i % kRing], 1);
     fence_mbar_init();
     tc::prefetch_tmap(&map_b0);
     tc::prefetch_tmap(&map_b1);
@@ -259,10 +333,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     // ================= TMA producer: activation tiles =================
     if (lane == 0) {
       int it = 0, ib = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const Item ti = item(tile);
+      for (int si = 0; si < plan.nseg; ++si) {
+        const Seg sg = plan.get(si);
+        const Item ti = item(sg.tile);
         const int m_blk = ti.m_blk, tok0 = ti.tok0;
-        for (int kb = 0; kb < a.n_kblk; ++kb, ++it) {
+        for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
           const int s = it % kStagesA;
           mbar_wait(&emptyA[s], ((it / kStagesA) & 1) ^ 1);
           // the weak block is already fp16/bf16 in 16 x 64 row-block tiles: TMA places it in
@@ -301,9 +376,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     const uint32_t idesc = tc::idesc_f16(std::is_same<T, __nv_bfloat16>::value, BM, BN,
                                          MODE == MODE_DGRAD, false);
     int it = 0, ib = 0, q0 = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int nsub = item(tile).nsub;
-      for (int kb = 0; kb < a.n_kblk; ++kb, ++it) {
+    for (int si = 0; si < plan.nseg; ++si) {
+      const Seg sg = plan.get(si);
+      const int nsub = item(sg.tile).nsub;
+      for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
         const int s = it % kStagesA;
         mbar_wait(&fullA[s], (it / kStagesA) & 1);
         tc::fence_after();
@@ -312,7 +388,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
         for (int j = 0; j < NSUB; ++j, ++ib) {
           if (j >= nsub) break;
           const int q = q0 + j, slot = q & 1;
-          if (kb == 0) {  // the epilogue has drained this slot's previous sub-tile
+          if (kb == sg.kb0) {  // the epilogue has drained this slot's previous sub-tile
             mbar_wait(&tempty_bar[slot], ((q >> 1) & 1) ^ 1);
             tc::fence_after();
           }
@@ -326,10 +402,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
               const uint64_t ad = (MODE == MODE_FWD) ? tc::smem_desc_sw128(a0 + 32 * k, 16, 1024)
                                                      : tc::smem_desc_sw128(a0 + 2048 * k, 8192, 1024);
               const uint64_t bd = tc::smem_desc_sw128(b0 + 32 * k, 16, 1024);
-              tc::mma_f16(tmem + slot * BN, ad, bd, idesc, (kb | k) ? 1u : 0u);
+              tc::mma_f16(tmem + slot * BN, ad, bd, idesc, (kb != sg.kb0 || k) ? 1u : 0u);
             }
             tc::commit(&emptyB[sb]);
-            if (kb == a.n_kblk - 1) tc::commit(&tfull_bar[slot]);
+            if (kb == sg.kb1 - 1) tc::commit(&tfull_bar[slot]);
           }
           __syncwarp();
         }
@@ -431,20 +507,30 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     };
     // flatten (tile, kb) into one stream so the prefetch crosses tile boundaries; the
     // stream is walked with incremental cursors (no integer divides per k-block)
-    const int per = a.n_kblk;
-    const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-    const int total = my_tiles * per;
+    int total = 0;
+    for (int si = 0; si < plan.nseg; ++si) {
+      const Seg sg = plan.get(si);
+      total += sg.kb1 - sg.kb0;
+    }
     struct Cursor {
-      int tile, m_blk, kb;
+      int si, m_blk, kb, kb1;
     };
-    auto advance = [&](Cursor& c) {
-      if (++c.kb == per) {
-        c.kb = 0;
-        c.tile += gridDim.x;
-        if (c.tile < ntiles) c.m_blk = item(c.tile).m_blk;  // once per tile
+    auto set_seg = [&](Cursor& c) {
+      if (c.si < plan.nseg) {
+        const Seg sg = plan.get(c.si);
+        c.m_blk = item(sg.tile).m_blk;  // once per segment
+        c.kb = sg.kb0;
+        c.kb1 = sg.kb1;
       }
     };
-    Cursor cl{(int)blockIdx.x, item(blockIdx.x).m_blk, 0};  // load cursor (2 ahead)
+    auto advance = [&](Cursor& c) {
+      if (++c.kb == c.kb1) {
+        ++c.si;
+        set_seg(c);
+      }
+    };
+    Cursor cl{0, 0, 0, 0};  // load cursor (2 ahead)
+    set_seg(cl);
     Cursor cp = cl;                                              // process cursor
     auto coords = [&](int, int& m_blk, int& kb) {  // next position of the load cursor
       m_blk = cl.m_blk;
@@ -485,9 +571,54 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     T* stg = sE + ew * 32 * kEpiStride;
     int q = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-    for (int j = 0; j < item(tile).nsub; ++j, ++q) {
-      const Item ti = item(tile);
+    const int erow = quad * 32 + lane;  // accumulator row of this thread
+    for (int si = 0; si < plan.nseg; ++si) {
+    const Seg sg = plan.get(si);
+    const Item ti = item(sg.tile);
+    // stream-K: a finisher of a tile begun by earlier CTAs waits for their partials, then streams
+    // them (4 KB per warp, cb and producer) through a per-warp ring of bulk copies in the stage
+    // memory -- free once the last sub-tile's MMAs are done, as the fix-up is the CTA's last
+    // segment. Partial layout per CTA: [sub-tile][cb][quad][c / 4][lane][4] fp32.
+    int p_lo = blockIdx.x;
+    const bool fixup = a.sk && sg.fin && sg.kb0 > 0;
+    constexpr int kCbChunk = 32 * 32 * 4;  // bytes of one warp's 32 rows x 32 columns
+    uint8_t* ring = sA + ew * kRing * kCbChunk;
+    int n_chunk = 0, c_use = 0;
+    auto chunk_src = [&](int c) {  // chunk c = (j, cb, producer) in consumption order
+      const int np = (int)blockIdx.x - p_lo;
+      const int p = p_lo + c % np, jc = c / np;
+      return (const uint8_t*)a.part +
+             ((size_t)p * (NSUB * BN * BM) + ((size_t)jc * 4 + quad) * 1024) * sizeof(float);
+    };
+    auto issue = [&](int c) {
+      const int slot = c % kRing;
+      mbar_expect_tx(&ring_full[ew][slot], kCbChunk);
+      bulk_g2s(ring + slot * kCbChunk, chunk_src(c), kCbChunk, &ring_full[ew][slot]);
+    };
+    if (fixup) {
+      const int64_t t0u = (int64_t)sg.tile * a.n_kblk;
+      p_lo = blockIdx.x - 1;
+      while (plan.start_of(p_lo) > t0u) --p_lo;
+      if (ew == 0 && lane == 0) {
+        for (int p = p_lo; p < (int)blockIdx.x; ++p) {
+          int f;
+          do {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(f) : "l"(a.flags + p) : "memory");
+          } while (f == 0);
+        }
+      }
+      named_bar_sync(1, kEpiWarps * 32);
+      // the stage memory is free when the tile's last sub-tile is accumulated
+      const int ql = q + ti.nsub - 1;
+      mbar_wait(&tfull_bar[ql & 1], (ql >> 1) & 1);
+      n_chunk = ti.nsub * (BN / 32) * ((int)blockIdx.x - p_lo);
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        for (int c = 0; c < min(n_chunk, kRing); ++c) issue(c);
+      }
+      __syncwarp();
+    }
+    for (int j = 0; j < ti.nsub; ++j, ++q) {
       const int m_blk = ti.m_blk;
       const int acc = q & 1;
       mbar_wait(&tfull_bar[acc], (q >> 1) & 1);
@@ -497,6 +628,35 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       for (int cb = 0; cb < BN / 32; ++cb) {
         uint32_t r[32];
         tc::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + acc * BN + cb * 32, r);
+        if (a.sk && !sg.fin) {
+          float4* dst = reinterpret_cast<float4*>(a.part + (size_t)blockIdx.x * (NSUB * BN * BM) +
+                                                  (((size_t)(j * (BN / 32) + cb) * 4 + quad) * 1024)) + lane;
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4)
+            __stcg(dst + c4 * 32, make_float4(__uint_as_float(r[4 * c4]), __uint_as_float(r[4 * c4 + 1]),
+                                              __uint_as_float(r[4 * c4 + 2]), __uint_as_float(r[4 * c4 + 3])));
+          continue;
+        }
+        if (fixup) {
+          for (int p = p_lo; p < (int)blockIdx.x; ++p, ++c_use) {
+            const int slot = c_use % kRing;
+            mbar_wait(&ring_full[ew][slot], (c_use / kRing) & 1);
+            const float4* src = reinterpret_cast<const float4*>(ring + slot * kCbChunk) + lane;
+#pragma unroll
+            for (int c4 = 0; c4 < 8; ++c4) {
+              const float4 v = src[c4 * 32];
+              r[4 * c4] = __float_as_uint(__uint_as_float(r[4 * c4]) + v.x);
+              r[4 * c4 + 1] = __float_as_uint(__uint_as_float(r[4 * c4 + 1]) + v.y);
+              r[4 * c4 + 2] = __float_as_uint(__uint_as_float(r[4 * c4 + 2]) + v.z);
+              r[4 * c4 + 3] = __float_as_uint(__uint_as_float(r[4 * c4 + 3]) + v.w);
+            }
+            __syncwarp();
+            if (lane == 0 && c_use + kRing < n_chunk) {
+              fence_proxy_async_smem();  // generic reads of the slot before the async overwrite
+              issue(c_use + kRing);
+            }
+          }
+        }
         // thread = one row (channel), 32 token columns -> staging [token][row]
 #pragma unroll
         for (int c = 0; c < 32; ++c) stg[c * kEpiStride + lane] = from_f32<T>(__uint_as_float(r[c]));
@@ -535,6 +695,19 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       tc::fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+    }
+    if (a.sk && !sg.fin) {
+      // publish this CTA's partial: every writer fences, then one release store
+      __threadfence();
+      named_bar_sync(1, kEpiWarps * 32);
+      if (ew == 0 && lane == 0)
+        asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(a.flags + blockIdx.x), "r"(1) : "memory");
+    } else if (a.sk && sg.fin && sg.kb0 > 0) {
+      // every epilogue warp is done reading the partials: re-arm the producers' flags
+      named_bar_sync(1, kEpiWarps * 32);
+      if (ew == 0 && lane == 0)
+        for (int p = p_lo; p < (int)blockIdx.x; ++p) a.flags[p] = 0;
+    }
     }
   }
 
@@ -796,11 +969,54 @@ int num_sms() {
   return n;
 }
 
+// stream-K scratch, one per (device, stream): flags[sms] (zero between launches: each finisher
+// re-arms the flags it consumed) + one fp32 partial tile (2 x 256 x 128) per CTA. Allocated on
+// first use outside graph capture; a capturing stream without one falls back to whole tiles.
+int g_sk_mode = getenv("QEFT_GEMM_SK") ? atoi(getenv("QEFT_GEMM_SK")) : -1;
+
+struct SkBuf {
+  float* part = nullptr;
+  int* flags = nullptr;
+};
+SkBuf sk_buffers(cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, SkBuf> bufs;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = bufs.find({dev, st});
+  if (it != bufs.end()) return it->second;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return SkBuf{};
+  }
+  const size_t bytes = 1024 + (size_t)num_sms() * 2 * 256 * BM * sizeof(float);
+  void* p = nullptr;
+  if (num_sms() > 256 || cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return SkBuf{};
+  }
+  if (cudaMemsetAsync(p, 0, 1024, st) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(p);
+    return SkBuf{};
+  }
+  SkBuf b;
+  b.flags = (int*)p;
+  b.part = (float*)((char*)p + 1024);
+  bufs[{dev, st}] = b;
+  return b;
+}
+
 template <int MODE, int BITS, typename T, int BN, int NSUB>
 int launch_gemm(const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& mw, const GemmArgs& a,
                 cudaStream_t st) {
   const size_t smem = GemmShape<BN, NSUB>::kSmem;
   static_assert(GemmShape<BN, NSUB>::kSmem <= 227 * 1024, "GEMM smem");
+  static_assert(kEpiWarps * kRing * 4096 <= GemmShape<BN, NSUB>::kStagesA * kStageA +
+                                                GemmShape<BN, NSUB>::kStagesB * GemmShape<BN, NSUB>::kStageB,
+                "stream-K fix-up ring fits the stage memory");
   auto kern = gemm_kernel<MODE, BITS, T, BN, NSUB>;
   static bool attr = false;
   if (!attr) {
@@ -810,15 +1026,35 @@ int launch_gemm(const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap&
   GemmArgs b = a;
   const int tiles = a.n_mblk * a.n_nblk, sms = num_sms();
   b.n_items = b.n_full = tiles;
+  double dp_span = (tiles + sms - 1) / sms;  // makespan of the round-robin schedule, in tile times
   if (NSUB == 2 && tiles > sms) {
     // split the last partial wave's tiles into halves when they then fit in one wave
     const int waves = (tiles + sms - 1) / sms, r = tiles - (waves - 1) * sms;
     if (r < sms && 2 * r <= sms) {
       b.n_full = (waves - 1) * sms;
       b.n_items = b.n_full + 2 * r;
+      dp_span = waves - 0.5;
     }
   }
-  const int grid = std::min(b.n_items, sms);
+  // stream-K when whole tiles leave SMs idle: every CTA gets tiles * n_kblk / sms k-blocks.
+  // Measured (profiles/r02/streamk_ab.json): it loses 4-12 % at 128 tiles on 148 SMs (two
+  // epilogues per CTA, the 256 KB partial store exposed while both TMEM slots are held), gains
+  // 2-3 % at 344 tiles, 27-50 % at 160 tiles and 30-70 % at 80 tiles (13B, T = 2048 / 512):
+  // worth it when it saves more than a tenth of a tile time
+  const int sk_mode = g_sk_mode;
+  const double sk_span = (double)tiles / sms + 0.06;
+  const int64_t units = (int64_t)tiles * a.n_kblk;
+  const bool sk_ok = sk_mode == 1 ? units >= sms : units >= 8LL * sms;
+  if (sk_mode != 0 && sk_ok && (sk_mode == 1 || sk_span + 0.1 < dp_span)) {
+    SkBuf sb = sk_buffers(st);
+    if (sb.part) {
+      b.sk = 1;
+      b.part = sb.part;
+      b.flags = sb.flags;
+      b.n_items = b.n_full = tiles;
+    }
+  }
+  const int grid = b.sk ? sms : std::min(b.n_items, sms);
   QEFT_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, m0, m1, mw, b));
   return 0;
 }
@@ -882,6 +1118,12 @@ int wgrad_splits(int oc, int T_) {
   int s = 1;
   while (s * 2 <= lim) s *= 2;
   return s;
+}
+
+int gemm_set_streamk(int mode) {
+  const int prev = g_sk_mode;
+  g_sk_mode = mode < 0 ? -1 : (mode > 0 ? 1 : 0);
+  return prev;
 }
 
 size_t gemm_workspace_bytes(const qeft_linear_t* L, int T_) {

@@ -63,6 +63,7 @@ int gemv2_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t l
                 int64_t ldy, int y_f32, int n, void* ws, size_t ws_bytes, cudaStream_t st);
 
 size_t gemm_workspace_bytes(const qeft_linear_t* L, int T);
+int gemm_set_streamk(int mode);
 int gemm_fwd(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ldy, int T,
              void* ws, size_t ws_bytes, cudaStream_t st);
 int gemm_dgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, void* dx, int64_t lddx, int T,

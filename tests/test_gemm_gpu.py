@@ -109,3 +109,52 @@ def test_train_golden_vs_reference(Q):
         assert rel_err(dx, z[p + "dx"]) <= TOL, t
         dw = dl.gemm_wgrad(dy, x).cpu().numpy()
         assert rel_err(dw, z[p + "dw"]) <= TOL, t
+
+
+# stream-K schedule: CTAs own contiguous k-block ranges; a tile split across CTAs is finished
+# by the CTA holding its last k-block, which adds the others' fp32 partials. Forced on, small
+# layers give every CTA a few k-blocks, so one tile spans many CTAs (multi-producer fix-ups).
+SK_CASES = [
+    (512, 1024, 128, 4, 128, "bf16", 256, "structured", False),   # 4 tiles x 18 k-blocks
+    (4096, 4096, 128, 4, 128, "f16", 2048, "structured", False),  # 128 tiles (the 7B shape)
+    (4096, 11008, 128, 4, 128, "f16", 2048, "structured", False),  # down_proj
+    (11008, 4096, 128, 4, 128, "f16", 2048, "structured", False),  # gate/up: 344 tiles
+    (256, 768, 64, 3, 128, "bf16", 700, "structured", False),
+    (160, 512, 16, 4, 32, "f16", 520, "irregular", False),
+    (128, 384, 32, 4, 64, "bf16", 1000, "structured", True),
+    (300, 2176, 64, 4, 64, "f16", 300, "structured", False),
+]
+
+
+@pytest.fixture
+def streamk():
+    from paper_2410_08661_b200 import _lib
+    L = _lib.lib()
+    prev = L.qeft_gemm_set_streamk(1)
+    yield L
+    L.qeft_gemm_set_streamk(prev)
+
+
+@pytest.mark.parametrize("case", SK_CASES)
+def test_streamk_matches_whole_tiles(Q, streamk, case):
+    import torch
+    oc, ic, k, bits, g, dt, T, layout, perm = case
+    q = _layer(Q, oc, ic, k, bits, g, layout, seed=oc + ic + 7, perm=perm)
+    dl = q.device(dt)
+    dq = dl.dequant_full().double()
+    x = torch.randn(T, ic, device="cuda").to(dl.tdtype)
+    dy = torch.randn(T, oc, device="cuda").to(dl.tdtype)
+    y_sk, dx_sk = dl.gemm_fwd(x), dl.gemm_dgrad(dy)
+    # deterministic: fixed partition, partials added in CTA order
+    assert torch.equal(dl.gemm_fwd(x), y_sk) and torch.equal(dl.gemm_dgrad(dy), dx_sk)
+    dx_acc = dl.gemm_dgrad(dy, out=dx_sk.clone(), accumulate=True)
+    streamk.qeft_gemm_set_streamk(0)
+    y_dp, dx_dp = dl.gemm_fwd(x), dl.gemm_dgrad(dy)
+    streamk.qeft_gemm_set_streamk(1)
+    ref, dref = x.double() @ dq.T, dy.double() @ dq
+    assert rel_err(y_sk.float().cpu().numpy(), ref.cpu().numpy()) <= TOL
+    assert rel_err(dx_sk.float().cpu().numpy(), dref.cpu().numpy()) <= TOL
+    assert rel_err(dx_acc.float().cpu().numpy(), 2 * dref.cpu().numpy()) <= TOL
+    # only the fp32 summation order differs from whole tiles: <= 2 output ulps
+    assert rel_err(y_sk.float().cpu().numpy(), y_dp.float().cpu().numpy()) <= 2e-3
+    assert rel_err(dx_sk.float().cpu().numpy(), dx_dp.float().cpu().numpy()) <= 2e-3
