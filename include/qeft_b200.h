@@ -143,12 +143,16 @@ int qeft_gemv_multi(const qeft_linear_t* const* layers, int n_layers, const void
  * wgrad: dw[o][j] (+)= sum_t dy[t][o] x[t][weak_j]   fp32 out       (qlinear_backward dW_weak)
  * workspace: qeft_gemm_workspace_bytes() (gather buffer for non-fast layouts). */
 size_t qeft_gemm_workspace_bytes(const qeft_linear_t* layer, int T);
-/* Tile schedule of the fwd / dgrad GEMMs: -1 = automatic (stream-K when whole 128 x 512 tiles
- * would leave SMs idle in the last wave), 0 = whole tiles only, 1 = stream-K whenever every SM
- * gets >= 1 k-block. Stream-K keeps one ~39 MB fp32 partial buffer per (device, stream),
- * allocated on first use outside CUDA-graph capture. Returns the previous mode. Process-wide;
- * QEFT_GEMM_SK in the environment sets the initial value. */
-int qeft_gemm_set_streamk(int mode);
+/* Tile schedule of the fwd / dgrad GEMMs (process-wide; returns the previous setting of `what`).
+ * what = QEFT_SCHED_STREAMK: -1 automatic (stream-K when whole tiles would leave SMs idle in
+ *   the last wave), 0 whole tiles only, 1 stream-K whenever every SM gets >= 1 k-block.
+ *   Stream-K keeps one ~39 MB fp32 partial buffer per (device, stream), allocated on first use
+ *   outside CUDA-graph capture. Initial value: QEFT_GEMM_SK.
+ * what = QEFT_SCHED_CTA_PAIRS: 1 one CTA per MMA tile (default), 2 CTA pairs (cta_group::2,
+ *   M = 256 over two SMs; even m-block counts, T > 128). Initial value: QEFT_GEMM_CG. */
+#define QEFT_SCHED_STREAMK 0
+#define QEFT_SCHED_CTA_PAIRS 1
+int qeft_gemm_set_schedule(int what, int value);
 int qeft_gemm_fwd(const qeft_linear_t* layer, const void* x, int64_t ldx, void* y, int64_t ldy,
                   int T, void* workspace, size_t workspace_bytes, void* stream);
 int qeft_gemm_dgrad(const qeft_linear_t* layer, const void* dy, int64_t lddy, void* dx,

@@ -121,7 +121,7 @@ int qeft_gemv_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64
 
 size_t qeft_gemm_workspace_bytes(const qeft_linear_t* L, int T) { return gemm_workspace_bytes(L, T); }
 
-int qeft_gemm_set_streamk(int mode) { return gemm_set_streamk(mode); }
+int qeft_gemm_set_schedule(int what, int value) { return gemm_set_schedule(what, value); }
 
 int qeft_gemm_fwd(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ldy, int T,
                   void* ws, size_t wsb, void* s) {

@@ -65,6 +65,11 @@ struct GemmArgs {
   int sk;
   float* part;
   int* flags;
+  unsigned long long* trace;  // profiling only (qeft_gemv_trace slots): per-CTA globaltimer stamps
+  int tma_out;     // epilogue writes 32 x 32 output blocks with TMA stores (reduce-add to accumulate)
+  int diag;  // profiling only (QEFT_GEMM_DIAG): 1 producers skip global loads, 2 skip dequant,
+             // 3 no MMAs, 4 no activation TMA after the first ring, 5 = 2 + 4 -- results are garbage;
+             // isolates the bounding pipeline
 };
 
 // The work of one CTA as a list of segments (tile, k-blocks [kb0, kb1)). Round-robin whole
@@ -80,8 +85,8 @@ struct SegPlan {
   int t_first, head, tail, nfull;
   int64_t u0, u1, U;
   QEFT_DEV static int64_t ustart(int64_t p, int64_t U, int G) { return p * U / G; }
-  QEFT_DEV void init(int ntiles, int nk_, int sk_) {
-    b = blockIdx.x; G = gridDim.x; nk = nk_; sk = sk_;
+  QEFT_DEV void init(int ntiles, int nk_, int sk_, int cg = 1) {
+    b = blockIdx.x / cg; G = gridDim.x / cg; nk = nk_; sk = sk_;  // a CTA pair shares one schedule
     if (!sk) {
       nseg = ntiles > b ? (ntiles - 1 - b) / G + 1 : 0;
       return;
@@ -247,20 +252,29 @@ QEFT_DEV void dequant_lane_general(const uint32_t* words, uint32_t hb, const flo
 // Ring depths: A stages (16 KB, dequantized / weak TMA) and B stages (BN x 64 activations).
 // A tile of NSUB sub-tiles reuses each A stage for NSUB MMA groups (N = BN each), so the
 // producers dequantize once per NSUB * BN tokens.
-template <int BN, int NSUB>
+// CG = 2: a CTA pair (cluster of 2) runs one M = 256 MMA over both SMs' shared memory: each CTA
+// dequantizes its own 128 rows of A and loads HALF of every B sub-tile (BN / 2 tokens), so the
+// per-SM shared-memory operand traffic per MMA drops from 12 KB to 8 KB (measured: the 1-SM
+// MMA of this kernel runs at ~58 % of the tcgen05 floor, shared-memory bound, with its producers
+// and activation TMA removed -- QEFT_GEMM_DIAG=5).
+template <int BN, int NSUB, int CG = 1>
 struct GemmShape {
-  static constexpr int kStageB = BN * BK * 2;
-  static constexpr int kStagesA = NSUB == 2 ? 3 : (BN == 256 ? 4 : 6);
-  static constexpr int kStagesB = NSUB == 2 ? 5 : kStagesA;
-  static constexpr size_t kSmem =
-      1024 + (size_t)kStagesA * kStageA + (size_t)kStagesB * kStageB + (size_t)kEpiWarps * 32 * kEpiStride * 2;
+  static constexpr int kStageB = (BN / CG) * BK * 2;
+  static constexpr int kStagesA = CG == 2 ? 4 : (NSUB == 2 ? 3 : (BN == 256 ? 4 : 6));
+  static constexpr int kStagesB = CG == 2 ? (NSUB == 2 ? 8 : 6) : (NSUB == 2 ? 5 : kStagesA);
+  // epilogue staging: 2 x [32 tokens][32 channels] per warp for TMA stores (>= the padded
+  // [32][kEpiStride] transpose buffer of the scalar path)
+  static constexpr size_t kEpiBytes = (size_t)kEpiWarps * 2 * 32 * 32 * 2;
+  static_assert(kEpiBytes >= (size_t)kEpiWarps * 32 * kEpiStride * 2, "staging");
+  static constexpr size_t kSmem = 1024 + (size_t)kStagesA * kStageA + (size_t)kStagesB * kStageB + kEpiBytes;
 };
 
-template <int MODE, int BITS, typename T, int BN, int NSUB>
+template <int MODE, int BITS, typename T, int BN, int NSUB, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ CUtensorMap map_b1,
-            const __grid_constant__ CUtensorMap map_w, const GemmArgs a) {
-  using Sh = GemmShape<BN, NSUB>;
+            const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_y,
+            const GemmArgs a) {
+  using Sh = GemmShape<BN, NSUB, CG>;
   constexpr int kStageB = Sh::kStageB;
   constexpr int kStagesA = Sh::kStagesA, kStagesB = Sh::kStagesB;
   // two accumulator slots of BN columns: sub-tile q (running count) uses slot q & 1
@@ -278,9 +292,21 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
   __shared__ uint32_t tmem_base;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * 8 : nullptr;
+  auto stamp = [&](int i) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[i] = t;
+  };
+  if (tr && threadIdx.x == 0) stamp(0);
   const int ntiles = a.n_items;
+  // CTA pair: rank 0 (leader) issues the MMAs; both CTAs produce their own A rows and B half
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
   SegPlan plan;
-  plan.init(ntiles, a.n_kblk, a.sk);
+  plan.init(ntiles, a.n_kblk, a.sk, CG);
+  // leader's copy of a barrier (shared::cluster address); the pair's producers arrive there
+  auto lead = [&](uint64_t* bar) -> uint32_t { return CG == 2 ? tc::mapa_u32(bar, 0) : smem_u32(bar); };
   // work item -> (m-block, first token, sub-tiles). Items past n_full are the halves of the
   // last partial wave's tiles, so that wave spreads over twice as many SMs.
   struct Item {
@@ -295,24 +321,25 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       half = (i - a.n_full) & 1;
       it.nsub = 1;
     }
-    const int n_blk = t / a.n_mblk;
-    it.m_blk = t - n_blk * a.n_mblk;
+    const int nm = CG == 2 ? a.n_mblk / 2 : a.n_mblk;  // pair tiles span two m-blocks
+    const int n_blk = t / nm;
+    it.m_blk = (t - n_blk * nm) * CG + (int)rank;
     it.tok0 = n_blk * kTileN + half * BN;
     return it;
   };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStagesA; ++s) {
-      mbar_init(&fullA[s], 1 + kProdWarps);  // TMA warp (weak bytes, maybe 0) + producers
+      mbar_init(&fullA[s], 1 + CG * kProdWarps);  // leader's TMA warp (weak bytes, maybe 0) + producers
       mbar_init(&emptyA[s], 1);
     }
     for (int s = 0; s < kStagesB; ++s) {
-      mbar_init(&fullB[s], 1);
+      mbar_init(&fullB[s], 1);  // the leader's TMA thread posts the pair's bytes
       mbar_init(&emptyB[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
-      mbar_init(&tempty_bar[i], kEpiWarps);
+      mbar_init(&tempty_bar[i], CG * kEpiWarps);
     }
     for (int i = 0; i < kEpiWarps * kRing; ++i) mbar_init(&ring_full[i / kRing][i % kRing], 1);
     fence_mbar_init();
@@ -320,14 +347,19 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     tc::prefetch_tmap(&map_b1);
     if (a.k) tc::prefetch_tmap(&map_w);
   }
-  if (warp == 1) tc::tmem_alloc(&tmem_base, kTmemCols);
+  if (warp == 1) {
+    if constexpr (CG == 2) tc::tmem_alloc_pair(&tmem_base, kTmemCols);
+    else tc::tmem_alloc(&tmem_base, kTmemCols);
+  }
   tc::fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();  // the peer's barriers are initialised before any remote arrive
   tc::fence_after();
   const uint32_t tmem = tmem_base;
 
   pdl_launch_dependents();
   pdl_wait();  // activations come from the previous kernel
+  if (tr && threadIdx.x == 0) stamp(1);
 
   if (warp == 0) {
     // ================= TMA producer: activation tiles =================
@@ -342,78 +374,111 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
           mbar_wait(&emptyA[s], ((it / kStagesA) & 1) ^ 1);
           // the weak block is already fp16/bf16 in 16 x 64 row-block tiles: TMA places it in
           // the A stage (SWIZZLE_128B, the layout the dequant producers write)
-          uint32_t wbytes = 0;
-          if (MODE == MODE_FWD && kb >= a.kq) wbytes = kStageA;
-          if (MODE == MODE_DGRAD && m_blk >= a.kq)
-            wbytes = (((m_blk - a.kq) * 2 + 1) * 64 < a.k_pad) ? kStageA : kStageA / 2;
-          mbar_expect_tx(&fullA[s], wbytes);
+          auto weak_bytes = [&](int mb) -> uint32_t {
+            if (MODE == MODE_FWD) return kb >= a.kq ? kStageA : 0;
+            if (mb < a.kq) return 0;
+            return (((mb - a.kq) * 2 + 1) * 64 < a.k_pad) ? kStageA : kStageA / 2;
+          };
+          const uint32_t wbytes = weak_bytes(m_blk);
+          auto load4 = [&](uint8_t* dst, int c2, int c3) {
+            if constexpr (CG == 2) tc::tma_load_4d_pair(dst, &map_w, 0, 0, c2, c3, lead(&fullA[s]));
+            else tc::tma_load_4d(dst, &map_w, 0, 0, c2, c3, &fullA[s]);
+          };
+          // a pair's leader posts both CTAs' weak bytes (the peer's m-block is m_blk + 1); the
+          // peer's copies may complete on the leader's barrier before this, which is allowed
+          if (leader) mbar_expect_tx(&fullA[s], CG == 2 ? wbytes + weak_bytes(m_blk + 1) : wbytes);
           if (MODE == MODE_FWD && kb >= a.kq) {
-            tc::tma_load_4d(sA + s * kStageA, &map_w, 0, 0, kb - a.kq, 8 * m_blk, &fullA[s]);
+            load4(sA + s * kStageA, kb - a.kq, 8 * m_blk);
           } else if (MODE == MODE_DGRAD && m_blk >= a.kq) {
             // MN-major A: two 64-row halves, one per weak K-tile (the second may be past k_pad)
             const int kw0 = (m_blk - a.kq) * 2;
-            tc::tma_load_4d(sA + s * kStageA, &map_w, 0, 0, kw0, 4 * kb, &fullA[s]);
-            if (wbytes == kStageA)
-              tc::tma_load_4d(sA + s * kStageA + 8192, &map_w, 0, 0, kw0 + 1, 4 * kb, &fullA[s]);
+            load4(sA + s * kStageA, kw0, 4 * kb);
+            if (wbytes == kStageA) load4(sA + s * kStageA + 8192, kw0 + 1, 4 * kb);
           }
 #pragma unroll
           for (int j = 0; j < NSUB; ++j, ++ib) {
             if (j >= ti.nsub) break;
             const int sb = ib % kStagesB;
             mbar_wait(&emptyB[sb], ((ib / kStagesB) & 1) ^ 1);
-            mbar_expect_tx(&fullB[sb], kStageB);
+            if ((a.diag == 4 || a.diag == 5) && ib >= kStagesB) {  // profiling: no activation traffic after the first ring
+              if (leader) mbar_arrive(&fullB[sb]);
+              continue;
+            }
             uint8_t* dst = sB + sb * kStageB;
-            if (MODE == MODE_FWD && !a.gathered && kb >= a.kq)
-              tc::tma_load_2d(dst, &map_b1, (kb - a.kq) * BK, tok0 + j * BN, &fullB[sb]);
-            else
-              tc::tma_load_2d(dst, &map_b0, kb * BK, tok0 + j * BN, &fullB[sb]);
+            const CUtensorMap* mb = (MODE == MODE_FWD && !a.gathered && kb >= a.kq) ? &map_b1 : &map_b0;
+            const int kc = (MODE == MODE_FWD && !a.gathered && kb >= a.kq) ? (kb - a.kq) * BK : kb * BK;
+            if constexpr (CG == 2) {  // this CTA's half of the sub-tile's tokens
+              if (leader) mbar_expect_tx(&fullB[sb], 2 * kStageB);
+              tc::tma_load_2d_pair(dst, mb, kc, tok0 + j * BN + (int)rank * (BN / 2), lead(&fullB[sb]));
+            } else {
+              mbar_expect_tx(&fullB[sb], kStageB);
+              tc::tma_load_2d(dst, mb, kc, tok0 + j * BN, &fullB[sb]);
+            }
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ================= MMA issuer (one thread) =================
-    const uint32_t idesc = tc::idesc_f16(std::is_same<T, __nv_bfloat16>::value, BM, BN,
+    // ================= MMA issuer (one thread; the leader CTA's for a pair) =================
+    if (!leader) goto mma_done;
+    {
+    const uint32_t idesc = tc::idesc_f16(std::is_same<T, __nv_bfloat16>::value, BM * CG, BN,
                                          MODE == MODE_DGRAD, false);
     int it = 0, ib = 0, q0 = 0;
+    auto wait = [&](uint64_t* bar, uint32_t par) { mbar_wait(bar, par); };
+    auto commit = [&](uint64_t* bar) {
+      if constexpr (CG == 2) tc::commit_pair(bar);
+      else tc::commit(bar);
+    };
     for (int si = 0; si < plan.nseg; ++si) {
       const Seg sg = plan.get(si);
       const int nsub = item(sg.tile).nsub;
       for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
         const int s = it % kStagesA;
-        mbar_wait(&fullA[s], (it / kStagesA) & 1);
+        wait(&fullA[s], (it / kStagesA) & 1);
         tc::fence_after();
         const uint32_t a0 = smem_u32(sA + s * kStageA);
+        // the CTA's last k-block: nobody waits for these stages again, and a pair's peer may
+        // already have left -- only the accumulator-full arrival is signalled
+        const bool last_kb = si == plan.nseg - 1 && kb == sg.kb1 - 1;
 #pragma unroll
         for (int j = 0; j < NSUB; ++j, ++ib) {
           if (j >= nsub) break;
           const int q = q0 + j, slot = q & 1;
           if (kb == sg.kb0) {  // the epilogue has drained this slot's previous sub-tile
-            mbar_wait(&tempty_bar[slot], ((q >> 1) & 1) ^ 1);
+            wait(&tempty_bar[slot], ((q >> 1) & 1) ^ 1);
             tc::fence_after();
           }
           const int sb = ib % kStagesB;
-          mbar_wait(&fullB[sb], (ib / kStagesB) & 1);
+          wait(&fullB[sb], (ib / kStagesB) & 1);
           tc::fence_after();
           if (lane == 0) {
             const uint32_t b0 = smem_u32(sB + sb * kStageB);
+            if (tr && it == 0 && j == 0) stamp(2);
+            if (tr && si == plan.nseg - 1 && kb == sg.kb1 - 1 && j == nsub - 1) stamp(3);
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
               const uint64_t ad = (MODE == MODE_FWD) ? tc::smem_desc_sw128(a0 + 32 * k, 16, 1024)
                                                      : tc::smem_desc_sw128(a0 + 2048 * k, 8192, 1024);
               const uint64_t bd = tc::smem_desc_sw128(b0 + 32 * k, 16, 1024);
-              tc::mma_f16(tmem + slot * BN, ad, bd, idesc, (kb != sg.kb0 || k) ? 1u : 0u);
+              const uint32_t acc = (kb != sg.kb0 || k) ? 1u : 0u;
+              if (a.diag != 3) {
+                if constexpr (CG == 2) tc::mma_f16_pair(tmem + slot * BN, ad, bd, idesc, acc);
+                else tc::mma_f16(tmem + slot * BN, ad, bd, idesc, acc);
+              }
             }
-            tc::commit(&emptyB[sb]);
-            if (kb == sg.kb1 - 1) tc::commit(&tfull_bar[slot]);
+            if (CG == 1 || !last_kb) commit(&emptyB[sb]);
+            if (kb == sg.kb1 - 1) commit(&tfull_bar[slot]);
           }
           __syncwarp();
         }
-        if (lane == 0) tc::commit(&emptyA[s]);
+        if (lane == 0 && (CG == 1 || !last_kb)) commit(&emptyA[s]);
         __syncwarp();
       }
       q0 += nsub;
     }
+    }
+  mma_done:;
   } else if (warp < 2 + kProdWarps) {
     // ================= dequant producers: the A operand =================
     // Each warp fills two 16-row x 64-column units of the A tile per k-block:
@@ -443,6 +508,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       }
     };
     auto load = [&](int m_blk, int kb, Pre& P) {
+      if (a.diag == 1) {
+#pragma unroll
+        for (int h = 0; h < kUPW; ++h) {
+          P.v[h] = make_uint4(lane * 0x01010101u, kb, m_blk, 7u);
+          P.p0[h] = P.p1[h] = make_float2(0.01f, 0.f);
+        }
+        return;
+      }
 #pragma unroll
       for (int h = 0; h < kUPW; ++h) {
         int rb, jt, kw;
@@ -558,12 +631,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       advance(cp);
       const int s = it % kStagesA;
       mbar_wait(&emptyA[s], ((it / kStagesA) & 1) ^ 1);
-      process(mb, kb, P0, sA + s * kStageA);
+      if (a.diag != 2 && a.diag != 5) process(mb, kb, P0, sA + s * kStageA);
+      if (tr && pw == 0 && lane == 0 && it == 0) stamp(6);
       P0 = P1;
       P1 = P2;
       fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
       __syncwarp();
-      if (lane == 0) mbar_arrive(&fullA[s]);
+      if (lane == 0) {
+        if constexpr (CG == 2) tc::mbar_arrive_cluster(lead(&fullA[s]));
+        else mbar_arrive(&fullA[s]);
+      }
     }
   } else {
     // ================= epilogue: TMEM -> registers -> smem transpose -> global =================
@@ -579,16 +656,19 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     // them (4 KB per warp, cb and producer) through a per-warp ring of bulk copies in the stage
     // memory -- free once the last sub-tile's MMAs are done, as the fix-up is the CTA's last
     // segment. Partial layout per CTA: [sub-tile][cb][quad][c / 4][lane][4] fp32.
-    int p_lo = blockIdx.x;
+    // schedule positions are per CTA pair (CG = 2); partials and flags per CTA: vid = p * CG + rank
+    const int pb = plan.b;
+    auto vid = [&](int pp) { return pp * CG + (int)rank; };
+    int p_lo = pb;
     const bool fixup = a.sk && sg.fin && sg.kb0 > 0;
     constexpr int kCbChunk = 32 * 32 * 4;  // bytes of one warp's 32 rows x 32 columns
     uint8_t* ring = sA + ew * kRing * kCbChunk;
     int n_chunk = 0, c_use = 0;
     auto chunk_src = [&](int c) {  // chunk c = (j, cb, producer) in consumption order
-      const int np = (int)blockIdx.x - p_lo;
+      const int np = pb - p_lo;
       const int p = p_lo + c % np, jc = c / np;
       return (const uint8_t*)a.part +
-             ((size_t)p * (NSUB * BN * BM) + ((size_t)jc * 4 + quad) * 1024) * sizeof(float);
+             ((size_t)vid(p) * (NSUB * BN * BM) + ((size_t)jc * 4 + quad) * 1024) * sizeof(float);
     };
     auto issue = [&](int c) {
       const int slot = c % kRing;
@@ -597,13 +677,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     };
     if (fixup) {
       const int64_t t0u = (int64_t)sg.tile * a.n_kblk;
-      p_lo = blockIdx.x - 1;
+      p_lo = pb - 1;
       while (plan.start_of(p_lo) > t0u) --p_lo;
       if (ew == 0 && lane == 0) {
-        for (int p = p_lo; p < (int)blockIdx.x; ++p) {
+        for (int p = p_lo; p < pb; ++p) {
           int f;
           do {
-            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(f) : "l"(a.flags + p) : "memory");
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(f) : "l"(a.flags + vid(p)) : "memory");
           } while (f == 0);
         }
       }
@@ -611,7 +691,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       // the stage memory is free when the tile's last sub-tile is accumulated
       const int ql = q + ti.nsub - 1;
       mbar_wait(&tfull_bar[ql & 1], (ql >> 1) & 1);
-      n_chunk = ti.nsub * (BN / 32) * ((int)blockIdx.x - p_lo);
+      n_chunk = ti.nsub * (BN / 32) * (pb - p_lo);
       if (lane == 0) {
         asm volatile("fence.proxy.async.global;\n" ::: "memory");
         for (int c = 0; c < min(n_chunk, kRing); ++c) issue(c);
@@ -623,22 +703,20 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       const int acc = q & 1;
       mbar_wait(&tfull_bar[acc], (q >> 1) & 1);
       tc::fence_after();
+      if (tr && ew == 0 && lane == 0 && q == 0) stamp(4);
       const int row_base = m_blk * BM + quad * 32;  // channel (fwd) / B200 column (dgrad) of lane 0
-#pragma unroll 1
-      for (int cb = 0; cb < BN / 32; ++cb) {
-        uint32_t r[32];
-        tc::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + acc * BN + cb * 32, r);
+      auto body = [&](int cb, uint32_t (&r)[32]) {
         if (a.sk && !sg.fin) {
-          float4* dst = reinterpret_cast<float4*>(a.part + (size_t)blockIdx.x * (NSUB * BN * BM) +
+          float4* dst = reinterpret_cast<float4*>(a.part + (size_t)vid(pb) * (NSUB * BN * BM) +
                                                   (((size_t)(j * (BN / 32) + cb) * 4 + quad) * 1024)) + lane;
 #pragma unroll
           for (int c4 = 0; c4 < 8; ++c4)
             __stcg(dst + c4 * 32, make_float4(__uint_as_float(r[4 * c4]), __uint_as_float(r[4 * c4 + 1]),
                                               __uint_as_float(r[4 * c4 + 2]), __uint_as_float(r[4 * c4 + 3])));
-          continue;
+          return;
         }
         if (fixup) {
-          for (int p = p_lo; p < (int)blockIdx.x; ++p, ++c_use) {
+          for (int p = p_lo; p < pb; ++p, ++c_use) {
             const int slot = c_use % kRing;
             mbar_wait(&ring_full[ew][slot], (c_use / kRing) & 1);
             const float4* src = reinterpret_cast<const float4*>(ring + slot * kCbChunk) + lane;
@@ -657,13 +735,46 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
             }
           }
         }
+        if (a.diag == 6) return;  // profiling: TMEM loads only
+        if (a.tma_out) {
+          // [32 tokens][32 channels] block -> one TMA store (clipped at the tensor's edges)
+          int col0 = row_base;
+          bool ok = true;
+          if (MODE == MODE_FWD) {
+            ok = row_base < a.oc;
+          } else if (row_base < a.m_pad) {
+            ok = row_base < a.m;  // [m, m_pad) is padding: its columns belong to the weak block
+          } else {
+            col0 = a.m + (row_base - a.m_pad);
+            ok = row_base - a.m_pad < a.k;
+          }
+          const int tc0 = ti.tok0 + j * BN + cb * 32;
+          ok = ok && tc0 < a.T;
+          T* buf = sE + (size_t)ew * 2048 + (cb & 1) * 1024;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");  // buffer free
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < 32; ++c) buf[c * 32 + lane] = from_f32<T>(__uint_as_float(r[c]));
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && ok) {
+            if (a.accumulate)
+              asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];\n"
+                           ::"l"(&map_y), "r"(col0), "r"(tc0), "r"(smem_u32(buf)) : "memory");
+            else
+              asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];\n"
+                           ::"l"(&map_y), "r"(col0), "r"(tc0), "r"(smem_u32(buf)) : "memory");
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+          }
+          return;
+        }
         // thread = one row (channel), 32 token columns -> staging [token][row]
 #pragma unroll
         for (int c = 0; c < 32; ++c) stg[c * kEpiStride + lane] = from_f32<T>(__uint_as_float(r[c]));
         __syncwarp();
         // thread = one token, 32 consecutive rows
         const int tok = ti.tok0 + j * BN + cb * 32 + lane;
-        if (tok < a.T) {
+        if (tok < a.T && a.diag != 7) {  // 7: profiling, no global stores
           const T* src = stg + lane * kEpiStride;
           if (MODE == MODE_FWD || a.fast_out) {
             int col0 = row_base;
@@ -691,31 +802,54 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
           }
         }
         __syncwarp();
+      };
+      // TMEM loads one column block ahead of the stores (BN / 32 is even)
+      const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + acc * BN;
+      uint32_t ra[32], rb[32];
+      tc::tmem_ld32_async(tbase, ra);
+      tc::tmem_wait_ld(ra);
+#pragma unroll 1
+      for (int cb = 0; cb < BN / 32; cb += 2) {
+        tc::tmem_ld32_async(tbase + (cb + 1) * 32, rb);
+        body(cb, ra);
+        tc::tmem_wait_ld(rb);
+        if (cb + 2 < BN / 32) tc::tmem_ld32_async(tbase + (cb + 2) * 32, ra);
+        body(cb + 1, rb);
+        if (cb + 2 < BN / 32) tc::tmem_wait_ld(ra);
       }
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2) tc::mbar_arrive_cluster(lead(&tempty_bar[acc]));
+        else mbar_arrive(&tempty_bar[acc]);
+      }
     }
     if (a.sk && !sg.fin) {
       // publish this CTA's partial: every writer fences, then one release store
       __threadfence();
       named_bar_sync(1, kEpiWarps * 32);
       if (ew == 0 && lane == 0)
-        asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(a.flags + blockIdx.x), "r"(1) : "memory");
+        asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(a.flags + vid(pb)), "r"(1) : "memory");
     } else if (a.sk && sg.fin && sg.kb0 > 0) {
       // every epilogue warp is done reading the partials: re-arm the producers' flags
       named_bar_sync(1, kEpiWarps * 32);
       if (ew == 0 && lane == 0)
-        for (int p = p_lo; p < (int)blockIdx.x; ++p) a.flags[p] = 0;
+        for (int p = p_lo; p < pb; ++p) a.flags[vid(p)] = 0;
     }
     }
   }
 
+  if (warp >= 2 + kProdWarps && lane == 0 && a.tma_out)
+    asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // output stores done before exit
+  if (tr && warp == 2 + kProdWarps && lane == 0) stamp(5);
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();  // both CTAs done: no arrivals in flight to the peer
   if (warp == 1) {
     tc::fence_after();
-    tc::tmem_dealloc(tmem, kTmemCols);
+    if constexpr (CG == 2) tc::tmem_dealloc_pair(tmem, kTmemCols);
+    else tc::tmem_dealloc(tmem, kTmemCols);
   }
+  if (tr && threadIdx.x == 0) stamp(7);
 }
 
 // ---------------------------------------------------------------------------
@@ -941,6 +1075,20 @@ int make_map(CUtensorMap* m, const void* base, int dtype, int64_t inner, int64_t
   return 0;
 }
 
+// output [rows][ld] tensor, box {32 columns, 32 rows}, no swizzle (epilogue TMA stores)
+int make_out_map(CUtensorMap* m, void* base, int dtype, int64_t inner, int64_t rows, int64_t ld_elems) {
+  auto fn = encode_fn();
+  if (fn == nullptr) return QEFT_ERR_CUDA;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld_elems * 2)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, dtype == QEFT_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base,
+                  dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : QEFT_ERR_CUDA;
+}
+
 // weak16 [oc_pad/16][k_pad/64][16][64] as a 4-D tensor, box {64, 16, 1, box_rb}, SWIZZLE_128B
 int make_weak_map(CUtensorMap* m, const void* weak16, int dtype, int k_pad, int n_rb, int box_rb) {
   auto fn = encode_fn();
@@ -973,6 +1121,10 @@ int num_sms() {
 // re-arms the flags it consumed) + one fp32 partial tile (2 x 256 x 128) per CTA. Allocated on
 // first use outside graph capture; a capturing stream without one falls back to whole tiles.
 int g_sk_mode = getenv("QEFT_GEMM_SK") ? atoi(getenv("QEFT_GEMM_SK")) : -1;
+// CTA pairs: implemented and parity-tested, not the default -- measured equal or 1-2 % slower
+// (profiles/r02/gemm_ab.json): this kernel's 1-SM MMA already runs at the cuBLAS per-SM rate
+// with its producers removed (QEFT_GEMM_DIAG=5), so halving B's per-SM traffic buys nothing
+int g_cg_mode = getenv("QEFT_GEMM_CG") ? (atoi(getenv("QEFT_GEMM_CG")) == 2 ? 2 : 1) : 1;
 
 struct SkBuf {
   float* part = nullptr;
@@ -1009,42 +1161,47 @@ SkBuf sk_buffers(cudaStream_t st) {
   return b;
 }
 
-template <int MODE, int BITS, typename T, int BN, int NSUB>
-int launch_gemm(const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& mw, const GemmArgs& a,
-                cudaStream_t st) {
-  const size_t smem = GemmShape<BN, NSUB>::kSmem;
-  static_assert(GemmShape<BN, NSUB>::kSmem <= 227 * 1024, "GEMM smem");
-  static_assert(kEpiWarps * kRing * 4096 <= GemmShape<BN, NSUB>::kStagesA * kStageA +
-                                                GemmShape<BN, NSUB>::kStagesB * GemmShape<BN, NSUB>::kStageB,
+template <int MODE, int BITS, typename T, int BN, int NSUB, int CG>
+int launch_gemm(const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& mw, const CUtensorMap& my,
+                const GemmArgs& a, cudaStream_t st) {
+  using Sh = GemmShape<BN, NSUB, CG>;
+  const size_t smem = Sh::kSmem;
+  static_assert(Sh::kSmem <= 227 * 1024, "GEMM smem");
+  static_assert(kEpiWarps * kRing * 4096 <= Sh::kStagesA * kStageA + Sh::kStagesB * Sh::kStageB,
                 "stream-K fix-up ring fits the stage memory");
-  auto kern = gemm_kernel<MODE, BITS, T, BN, NSUB>;
+  auto kern = gemm_kernel<MODE, BITS, T, BN, NSUB, CG>;
   static bool attr = false;
   if (!attr) {
     QEFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   GemmArgs b = a;
-  const int tiles = a.n_mblk * a.n_nblk, sms = num_sms();
+  static const int diag = getenv("QEFT_GEMM_DIAG") ? atoi(getenv("QEFT_GEMM_DIAG")) : 0;
+  b.diag = diag;
+  b.trace = trace_next_slot();
+  // workers: CTAs, or CTA pairs (CG = 2: a tile is 256 rows = two m-blocks)
+  const int sms = num_sms(), workers = sms / CG;
+  const int tiles = (a.n_mblk / CG) * a.n_nblk;
   b.n_items = b.n_full = tiles;
-  double dp_span = (tiles + sms - 1) / sms;  // makespan of the round-robin schedule, in tile times
-  if (NSUB == 2 && tiles > sms) {
+  double dp_span = (tiles + workers - 1) / workers;  // makespan of the round-robin schedule, in tile times
+  if (NSUB == 2 && tiles > workers) {
     // split the last partial wave's tiles into halves when they then fit in one wave
-    const int waves = (tiles + sms - 1) / sms, r = tiles - (waves - 1) * sms;
-    if (r < sms && 2 * r <= sms) {
-      b.n_full = (waves - 1) * sms;
+    const int waves = (tiles + workers - 1) / workers, r = tiles - (waves - 1) * workers;
+    if (r < workers && 2 * r <= workers) {
+      b.n_full = (waves - 1) * workers;
       b.n_items = b.n_full + 2 * r;
       dp_span = waves - 0.5;
     }
   }
-  // stream-K when whole tiles leave SMs idle: every CTA gets tiles * n_kblk / sms k-blocks.
-  // Measured (profiles/r02/streamk_ab.json): it loses 4-12 % at 128 tiles on 148 SMs (two
-  // epilogues per CTA, the 256 KB partial store exposed while both TMEM slots are held), gains
-  // 2-3 % at 344 tiles, 27-50 % at 160 tiles and 30-70 % at 80 tiles (13B, T = 2048 / 512):
-  // worth it when it saves more than a tenth of a tile time
+  // stream-K when whole tiles leave SMs idle: every worker gets tiles * n_kblk / workers
+  // k-blocks. Measured (profiles/r02/streamk_ab.json, 1-SM tiles): it loses 4-12 % at 128 tiles
+  // on 148 SMs (two epilogues per CTA, the 256 KB partial store exposed while both TMEM slots
+  // are held), gains 2-3 % at 344 tiles, 27-50 % at 160 tiles and 30-70 % at 80 tiles (13B,
+  // T = 2048 / 512): worth it when it saves more than a tenth of a tile time
   const int sk_mode = g_sk_mode;
-  const double sk_span = (double)tiles / sms + 0.06;
+  const double sk_span = (double)tiles / workers + 0.06;
   const int64_t units = (int64_t)tiles * a.n_kblk;
-  const bool sk_ok = sk_mode == 1 ? units >= sms : units >= 8LL * sms;
+  const bool sk_ok = sk_mode == 1 ? units >= workers : units >= 8LL * workers;
   if (sk_mode != 0 && sk_ok && (sk_mode == 1 || sk_span + 0.1 < dp_span)) {
     SkBuf sb = sk_buffers(st);
     if (sb.part) {
@@ -1054,27 +1211,41 @@ int launch_gemm(const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap&
       b.n_items = b.n_full = tiles;
     }
   }
-  const int grid = b.sk ? sms : std::min(b.n_items, sms);
-  QEFT_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, m0, m1, mw, b));
+  const int grid = CG * (b.sk ? workers : std::min(b.n_items, workers));
+  if (CG == 2) {
+    QEFT_CUDA(launch_pdl_cluster(kern, dim3(grid), dim3(kThreads), smem, st, 2, m0, m1, mw, my, b));
+  } else {
+    QEFT_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, m0, m1, mw, my, b));
+  }
   return 0;
 }
 
-template <int MODE, typename T>
-int dispatch_gemm(const qeft_linear_t* L, int T_, const CUtensorMap& m0, const CUtensorMap& m1, GemmArgs& a,
-                  cudaStream_t st) {
+// Tile plan of one GEMM: N per sub-tile (BN), sub-tiles sharing each dequantized A stage (NSUB),
+// CTAs per MMA (CG). The activation maps' box is BN / CG tokens.
+struct GemmPlan {
+  int bn, nsub, cg;
+};
+GemmPlan gemm_plan(int n_mblk, int T_) {
   // tile N: 128 tokens (T <= 128), 256, or 2 x 256 sharing each dequantized A stage (T > 256;
   // QEFT_GEMM_NSUB=1 forces single sub-tiles)
-  static const int nsub_env = [] {
-    const char* e = getenv("QEFT_GEMM_NSUB");
-    return e ? atoi(e) : 0;
-  }();
+  static const int nsub_env = getenv("QEFT_GEMM_NSUB") ? atoi(getenv("QEFT_GEMM_NSUB")) : 0;
+  GemmPlan p;
   const bool big = T_ > 128;
   // paired sub-tiles halve dequant work per FLOP, but when even twice the items of single
   // sub-tiles fit one wave (few m-blocks, short T: 13B T=512), parallelism wins
-  const int pair_items = a.n_mblk * ((T_ + 511) / 512);
-  const bool pair = T_ > 256 && nsub_env != 1 && 2 * pair_items > num_sms();
-  const int BN = big ? 256 : 128;
-  a.n_nblk = (T_ + BN * (pair ? 2 : 1) - 1) / (BN * (pair ? 2 : 1));
+  const int pair_items = n_mblk * ((T_ + 511) / 512);
+  p.nsub = (T_ > 256 && nsub_env != 1 && 2 * pair_items > num_sms()) ? 2 : 1;
+  p.bn = big ? 256 : 128;
+  // CTA pairs (M = 256) for 256-token sub-tiles over an even number of m-blocks
+  p.cg = (big && n_mblk % 2 == 0 && g_cg_mode == 2) ? 2 : 1;
+  return p;
+}
+
+template <int MODE, typename T>
+int dispatch_gemm(const qeft_linear_t* L, int T_, const GemmPlan& p, const CUtensorMap& m0, const CUtensorMap& m1,
+                  GemmArgs& a, cudaStream_t st) {
+  const bool pair = p.nsub == 2, big = p.bn == 256;
+  a.n_nblk = (T_ + p.bn * p.nsub - 1) / (p.bn * p.nsub);
   // weak block as a 4-D tensor {64 columns, 16 rows, k_pad/64 tiles, row-blocks} of the
   // row-block tile layout (weak_off, qeft_common.cuh); box = 8 row-blocks (fwd: the 128 rows of
   // the K-major A tile) or 4 row-blocks (dgrad: one 64-row half of the MN-major A tile)
@@ -1083,12 +1254,27 @@ int dispatch_gemm(const qeft_linear_t* L, int T_, const CUtensorMap& m0, const C
     if (int r = make_weak_map(&mw, L->weak16, L->act_dtype, L->k_pad, L->oc_pad / 16, MODE == MODE_FWD ? 8 : 4))
       return r;
   }
-  if (L->bits == 4) {
-    if (pair) return launch_gemm<MODE, 4, T, 256, 2>(m0, m1, mw, a, st);
-    return big ? launch_gemm<MODE, 4, T, 256, 1>(m0, m1, mw, a, st) : launch_gemm<MODE, 4, T, 128, 1>(m0, m1, mw, a, st);
+  // output blocks by TMA store: contiguous output columns (fwd, or dgrad's structured layout),
+  // 16-byte aligned rows (QEFT_GEMM_TMA_OUT=0: per-thread stores through a padded transpose)
+  static const int tma_env = getenv("QEFT_GEMM_TMA_OUT") ? atoi(getenv("QEFT_GEMM_TMA_OUT")) : 1;
+  CUtensorMap my = m0;
+  a.tma_out = 0;
+  if (tma_env && (MODE == MODE_FWD || a.fast_out) && (a.ldo * 2) % 16 == 0 &&
+      ((uintptr_t)a.out & 15) == 0) {
+    if (make_out_map(&my, a.out, L->act_dtype, a.out_cols, T_, a.ldo) == 0) a.tma_out = 1;
   }
-  if (pair) return launch_gemm<MODE, 3, T, 256, 2>(m0, m1, mw, a, st);
-  return big ? launch_gemm<MODE, 3, T, 256, 1>(m0, m1, mw, a, st) : launch_gemm<MODE, 3, T, 128, 1>(m0, m1, mw, a, st);
+#define QEFT_GL(B)                                                                                    \
+  if (p.cg == 2) {                                                                                    \
+    if (pair) return launch_gemm<MODE, B, T, 256, 2, 2>(m0, m1, mw, my, a, st);                            \
+    return launch_gemm<MODE, B, T, 256, 1, 2>(m0, m1, mw, my, a, st);                                      \
+  }                                                                                                   \
+  if (pair) return launch_gemm<MODE, B, T, 256, 2, 1>(m0, m1, mw, my, a, st);                              \
+  return big ? launch_gemm<MODE, B, T, 256, 1, 1>(m0, m1, mw, my, a, st) : launch_gemm<MODE, B, T, 128, 1, 1>(m0, m1, mw, my, a, st);
+  if (L->bits == 4) {
+    QEFT_GL(4)
+  }
+  QEFT_GL(3)
+#undef QEFT_GL
 }
 
 GemmArgs base_args(const qeft_linear_t* L, int T_) {
@@ -1120,10 +1306,19 @@ int wgrad_splits(int oc, int T_) {
   return s;
 }
 
-int gemm_set_streamk(int mode) {
-  const int prev = g_sk_mode;
-  g_sk_mode = mode < 0 ? -1 : (mode > 0 ? 1 : 0);
-  return prev;
+int gemm_set_schedule(int what, int value) {
+  if (what == QEFT_SCHED_STREAMK) {
+    const int prev = g_sk_mode;
+    g_sk_mode = value < 0 ? -1 : (value > 0 ? 1 : 0);
+    return prev;
+  }
+  if (what == QEFT_SCHED_CTA_PAIRS) {
+    const int prev = g_cg_mode;
+    g_cg_mode = value == 2 ? 2 : 1;
+    return prev;
+  }
+  set_error("gemm_set_schedule: unknown setting %d", what);
+  return QEFT_ERR_SHAPE;
 }
 
 size_t gemm_workspace_bytes(const qeft_linear_t* L, int T_) {
@@ -1160,7 +1355,8 @@ int gemm_fwd(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_
   a.out_cols = L->oc;
   CUtensorMap m0, m1;
   const bool fast = (L->flags & QEFT_FLAG_STRUCTURED_FAST) && ldx % 8 == 0 && ((uintptr_t)x & 15) == 0;
-  const int box = T_ > 128 ? 256 : 128;
+  const GemmPlan plan = gemm_plan(a.n_mblk, T_);
+  const int box = plan.bn / plan.cg;
   if (fast) {
     if (int r = make_map(&m0, x, L->act_dtype, L->m, T_, ldx, box)) return r;
     const void* xw = (const char*)x + (size_t)L->m * 2;
@@ -1173,8 +1369,8 @@ int gemm_fwd(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_
     m1 = m0;
     a.gathered = 1;
   }
-  if (L->act_dtype == QEFT_F16) return dispatch_gemm<MODE_FWD, __half>(L, T_, m0, m1, a, st);
-  return dispatch_gemm<MODE_FWD, __nv_bfloat16>(L, T_, m0, m1, a, st);
+  if (L->act_dtype == QEFT_F16) return dispatch_gemm<MODE_FWD, __half>(L, T_, plan, m0, m1, a, st);
+  return dispatch_gemm<MODE_FWD, __nv_bfloat16>(L, T_, plan, m0, m1, a, st);
 }
 
 int gemm_dgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, void* dx, int64_t lddx, int T_,
@@ -1192,10 +1388,10 @@ int gemm_dgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, void* dx, i
   a.out_cols = L->ic;
   a.fast_out = (L->flags & QEFT_FLAG_STRUCTURED_FAST) && (L->m % 32 == 0);
   CUtensorMap m0;
-  const int box = T_ > 128 ? 256 : 128;
-  if (int r = make_map(&m0, dy, L->act_dtype, L->oc, T_, lddy, box)) return r;
-  if (L->act_dtype == QEFT_F16) return dispatch_gemm<MODE_DGRAD, __half>(L, T_, m0, m0, a, st);
-  return dispatch_gemm<MODE_DGRAD, __nv_bfloat16>(L, T_, m0, m0, a, st);
+  const GemmPlan plan = gemm_plan(a.n_mblk, T_);
+  if (int r = make_map(&m0, dy, L->act_dtype, L->oc, T_, lddy, plan.bn / plan.cg)) return r;
+  if (L->act_dtype == QEFT_F16) return dispatch_gemm<MODE_DGRAD, __half>(L, T_, plan, m0, m0, a, st);
+  return dispatch_gemm<MODE_DGRAD, __nv_bfloat16>(L, T_, plan, m0, m0, a, st);
 }
 
 template <typename T, int NW>

@@ -20,6 +20,11 @@ static unsigned long long* g_trace = nullptr;
 static int g_trace_slots = 0, g_trace_next = 0;
 constexpr int kTraceCtas = 512;
 
+unsigned long long* trace_next_slot() {
+  if (g_trace && g_trace_next < g_trace_slots) return g_trace + (size_t)(g_trace_next++) * kTraceCtas * 8;
+  return nullptr;
+}
+
 int gemv_trace(int slots, unsigned long long* host_out) {
   if (slots > 0) {  // arm: allocate and clear
     if (g_trace) cudaFree(g_trace);
@@ -76,7 +81,7 @@ int gemv2_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t l
   static const int contig = env_int("QEFT_GEMV2_CONTIG", 1);
   a.contig = contig;
   a.trace = nullptr;
-  if (g_trace && g_trace_next < g_trace_slots) a.trace = g_trace + (size_t)(g_trace_next++) * kTraceCtas * 8;
+  a.trace = trace_next_slot();
   const int gt = L->g / 64;
   const bool bf = L->act_dtype == QEFT_BF16;
   if (L->bits == 4) return bf ? dispatch_4b(a, gt, st) : dispatch_4h(a, gt, st);

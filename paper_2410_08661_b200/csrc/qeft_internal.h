@@ -57,13 +57,15 @@ int gemv_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ld
 // bulk-copy warp-ring GEMV (qeft_gemv2.cu); gemv2_multi returns -1 when the launch needs the
 // generic path (its partials would not fit shared memory)
 int gemv_trace(int slots, unsigned long long* host_out);
+// next armed trace slot (512 CTAs x 8 u64) of qeft_gemv_trace, or null: GEMV and GEMM launches
+unsigned long long* trace_next_slot();
 bool gemv2_supported(const qeft_linear_t* L, int n);
 size_t gemv2_workspace_bytes(const qeft_linear_t* L, int n);
 int gemv2_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ldx, void* const* ys,
                 int64_t ldy, int y_f32, int n, void* ws, size_t ws_bytes, cudaStream_t st);
 
 size_t gemm_workspace_bytes(const qeft_linear_t* L, int T);
-int gemm_set_streamk(int mode);
+int gemm_set_schedule(int what, int value);
 int gemm_fwd(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ldy, int T,
              void* ws, size_t ws_bytes, cudaStream_t st);
 int gemm_dgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, void* dx, int64_t lddx, int T,

@@ -31,7 +31,7 @@ class _QEFTLinearFn(torch.autograd.Function):
         y = dl.gemv(x2) if use_gemv else dl.gemm_fwd(x2)
         ctx.mod = mod
         if weak32.requires_grad and dl.k:
-            ctx.save_for_backward(dl.gather_weak(x2))
+            ctx.save_for_backward(_weak_slice(dl, x2))
         else:
             ctx.save_for_backward(None)
         return y
@@ -55,6 +55,18 @@ class _QEFTLinearFn(torch.autograd.Function):
             if mod.grad_ready_hook is not None:  # e.g. launch this layer group's DP all-reduce
                 mod.grad_ready_hook(mod)
         return dx, None, None, None
+
+
+def _weak_slice(dl: DeviceLayer, x2):
+    """x_weak for the backward (TrainableLayerState.x_weak, tuning.py:30-34, 70-71). Structured
+    layers hold their weak block in the trailing input columns [m, ic): the wgrad GEMM reads
+    that strided view of x in place by TMA (row pitch ic), so no copy is made and no kernel
+    launched -- the role the GEMM epilogue would otherwise play. Other layouts gather the k
+    weak columns (one small launch)."""
+    if (dl.structured_fast and x2.stride(1) == 1 and x2.stride(0) % 8 == 0 and dl.m % 8 == 0
+            and x2.data_ptr() % 16 == 0 and x2.shape[0] > 1):
+        return x2[:, dl.m:dl.m + dl.k]
+    return dl.gather_weak(x2)
 
 
 class QEFTLinear(torch.nn.Module):

@@ -114,6 +114,11 @@ def test_train_golden_vs_reference(Q):
 # stream-K schedule: CTAs own contiguous k-block ranges; a tile split across CTAs is finished
 # by the CTA holding its last k-block, which adds the others' fp32 partials. Forced on, small
 # layers give every CTA a few k-blocks, so one tile spans many CTAs (multi-producer fix-ups).
+def _ulp2(dt):
+    """Two output rounding steps of the activation dtype, relative to the largest output."""
+    return 2.0 * (2.0 ** -10 if dt == "f16" else 2.0 ** -7)
+
+
 SK_CASES = [
     (512, 1024, 128, 4, 128, "bf16", 256, "structured", False),   # 4 tiles x 18 k-blocks
     (4096, 4096, 128, 4, 128, "f16", 2048, "structured", False),  # 128 tiles (the 7B shape)
@@ -126,13 +131,16 @@ SK_CASES = [
 ]
 
 
+SK, PAIRS = 0, 1  # QEFT_SCHED_STREAMK, QEFT_SCHED_CTA_PAIRS
+
+
 @pytest.fixture
 def streamk():
     from paper_2410_08661_b200 import _lib
     L = _lib.lib()
-    prev = L.qeft_gemm_set_streamk(1)
+    prev = L.qeft_gemm_set_schedule(SK, 1)
     yield L
-    L.qeft_gemm_set_streamk(prev)
+    L.qeft_gemm_set_schedule(SK, prev)
 
 
 @pytest.mark.parametrize("case", SK_CASES)
@@ -148,13 +156,48 @@ def test_streamk_matches_whole_tiles(Q, streamk, case):
     # deterministic: fixed partition, partials added in CTA order
     assert torch.equal(dl.gemm_fwd(x), y_sk) and torch.equal(dl.gemm_dgrad(dy), dx_sk)
     dx_acc = dl.gemm_dgrad(dy, out=dx_sk.clone(), accumulate=True)
-    streamk.qeft_gemm_set_streamk(0)
+    streamk.qeft_gemm_set_schedule(SK, 0)
     y_dp, dx_dp = dl.gemm_fwd(x), dl.gemm_dgrad(dy)
-    streamk.qeft_gemm_set_streamk(1)
+    streamk.qeft_gemm_set_schedule(SK, 1)
     ref, dref = x.double() @ dq.T, dy.double() @ dq
     assert rel_err(y_sk.float().cpu().numpy(), ref.cpu().numpy()) <= TOL
     assert rel_err(dx_sk.float().cpu().numpy(), dref.cpu().numpy()) <= TOL
     assert rel_err(dx_acc.float().cpu().numpy(), 2 * dref.cpu().numpy()) <= TOL
     # only the fp32 summation order differs from whole tiles: <= 2 output ulps
-    assert rel_err(y_sk.float().cpu().numpy(), y_dp.float().cpu().numpy()) <= 2e-3
-    assert rel_err(dx_sk.float().cpu().numpy(), dx_dp.float().cpu().numpy()) <= 2e-3
+    ulp2 = _ulp2(dt)
+    assert rel_err(y_sk.float().cpu().numpy(), y_dp.float().cpu().numpy()) <= ulp2
+    assert rel_err(dx_sk.float().cpu().numpy(), dx_dp.float().cpu().numpy()) <= ulp2
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c[6] > 128] + SK_CASES[1:4])
+@pytest.mark.parametrize("sk", [0, 1])
+def test_cta_pairs_match_single(Q, case, sk):
+    """cta_group::2 tiles (M = 256 over two SMs; each CTA dequantizes its own 128 rows and loads
+    half of every activation sub-tile; the leader issues the MMAs) against the 1-SM kernel and
+    the fp64 product, with whole tiles and with stream-K over CTA pairs."""
+    import torch
+    from paper_2410_08661_b200 import _lib
+    L = _lib.lib()
+    oc, ic, k, bits, g, dt, T, layout, perm = case
+    q = _layer(Q, oc, ic, k, bits, g, layout, seed=oc + ic + 11, perm=perm)
+    dl = q.device(dt)
+    dq = dl.dequant_full().double()
+    x = torch.randn(T, ic, device="cuda").to(dl.tdtype)
+    dy = torch.randn(T, oc, device="cuda").to(dl.tdtype)
+    prev_sk = L.qeft_gemm_set_schedule(SK, sk)
+    try:
+        y1, dx1 = dl.gemm_fwd(x), dl.gemm_dgrad(dy)
+        prev = L.qeft_gemm_set_schedule(PAIRS, 2)
+        try:
+            y2, dx2 = dl.gemm_fwd(x), dl.gemm_dgrad(dy)
+            dx2a = dl.gemm_dgrad(dy, out=dx2.clone(), accumulate=True)
+        finally:
+            L.qeft_gemm_set_schedule(PAIRS, prev)
+    finally:
+        L.qeft_gemm_set_schedule(SK, prev_sk)
+    ref, dref = x.double() @ dq.T, dy.double() @ dq
+    assert rel_err(y2.float().cpu().numpy(), ref.cpu().numpy()) <= TOL
+    assert rel_err(dx2.float().cpu().numpy(), dref.cpu().numpy()) <= TOL
+    assert rel_err(dx2a.float().cpu().numpy(), 2 * dref.cpu().numpy()) <= TOL
+    assert rel_err(y2.float().cpu().numpy(), y1.float().cpu().numpy()) <= _ulp2(dt)
+    assert rel_err(dx2.float().cpu().numpy(), dx1.float().cpu().numpy()) <= _ulp2(dt)
