@@ -29,6 +29,10 @@
 
 using namespace qeft;
 
+#ifndef QEFT_GEMM_PROFILE
+#define QEFT_GEMM_PROFILE 0  // 1: per-CTA globaltimer stamps + QEFT_GEMM_DIAG modes (scripts/trace_gemm.py)
+#endif
+
 namespace {
 
 enum { MODE_FWD = 0, MODE_DGRAD = 1 };
@@ -80,14 +84,15 @@ struct GemmArgs {
 struct Seg {
   int tile, kb0, kb1, fin;
 };
+template <bool SK>
 struct SegPlan {
   int nseg, b, G, nk, sk;
   int t_first, head, tail, nfull;
   int64_t u0, u1, U;
   QEFT_DEV static int64_t ustart(int64_t p, int64_t U, int G) { return p * U / G; }
-  QEFT_DEV void init(int ntiles, int nk_, int sk_, int cg = 1) {
-    b = blockIdx.x / cg; G = gridDim.x / cg; nk = nk_; sk = sk_;  // a CTA pair shares one schedule
-    if (!sk) {
+  QEFT_DEV void init(int ntiles, int nk_, int cg = 1) {
+    b = blockIdx.x / cg; G = gridDim.x / cg; nk = nk_; sk = SK;  // a CTA pair shares one schedule
+    if constexpr (!SK) {
       nseg = ntiles > b ? (ntiles - 1 - b) / G + 1 : 0;
       return;
     }
@@ -107,7 +112,7 @@ struct SegPlan {
   }
   QEFT_DEV Seg get(int i) const {
     Seg s;
-    if (!sk) {
+    if constexpr (!SK) {
       s.tile = b + i * G; s.kb0 = 0; s.kb1 = nk; s.fin = 1;
       return s;
     }
@@ -269,7 +274,7 @@ struct GemmShape {
   static constexpr size_t kSmem = 1024 + (size_t)kStagesA * kStageA + (size_t)kStagesB * kStageB + kEpiBytes;
 };
 
-template <int MODE, int BITS, typename T, int BN, int NSUB, int CG>
+template <int MODE, int BITS, typename T, int BN, int NSUB, int CG, bool SKT>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ CUtensorMap map_b1,
             const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_y,
@@ -292,19 +297,33 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
   __shared__ uint32_t tmem_base;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if QEFT_GEMM_PROFILE
   unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * 8 : nullptr;
+#else
+  constexpr unsigned long long* tr = nullptr;  // profiling build only (make EXTRA=-DQEFT_GEMM_PROFILE=1)
+#endif
   auto stamp = [&](int i) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    tr[i] = t;
+    if constexpr (QEFT_GEMM_PROFILE) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[(size_t)blockIdx.x * 8 + i] = t;
+    }
   };
   if (tr && threadIdx.x == 0) stamp(0);
   const int ntiles = a.n_items;
+#if QEFT_GEMM_PROFILE
+  const int DIAG_ = a.diag;
+#else
+  constexpr int DIAG_ = 0;
+#endif
   // CTA pair: rank 0 (leader) issues the MMAs; both CTAs produce their own A rows and B half
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
   const bool leader = rank == 0;
-  SegPlan plan;
-  plan.init(ntiles, a.n_kblk, a.sk, CG);
+  // whole tiles (SKT = false: the schedule and the producers' cursor are the plain tile-stride
+  // loop) or stream-K segments -- separate instantiations, so the whole-tile kernel carries none
+  // of the stream-K bookkeeping in registers
+  SegPlan<SKT> plan;
+  plan.init(ntiles, a.n_kblk, CG);
   // leader's copy of a barrier (shared::cluster address); the pair's producers arrive there
   auto lead = [&](uint64_t* bar) -> uint32_t { return CG == 2 ? tc::mapa_u32(bar, 0) : smem_u32(bar); };
   // work item -> (m-block, first token, sub-tiles). Items past n_full are the halves of the
@@ -400,7 +419,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
             if (j >= ti.nsub) break;
             const int sb = ib % kStagesB;
             mbar_wait(&emptyB[sb], ((ib / kStagesB) & 1) ^ 1);
-            if ((a.diag == 4 || a.diag == 5) && ib >= kStagesB) {  // profiling: no activation traffic after the first ring
+            if ((DIAG_ == 4 || DIAG_ == 5) && ib >= kStagesB) {  // profiling: no activation traffic after the first ring
               if (leader) mbar_arrive(&fullB[sb]);
               continue;
             }
@@ -462,7 +481,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
                                                      : tc::smem_desc_sw128(a0 + 2048 * k, 8192, 1024);
               const uint64_t bd = tc::smem_desc_sw128(b0 + 32 * k, 16, 1024);
               const uint32_t acc = (kb != sg.kb0 || k) ? 1u : 0u;
-              if (a.diag != 3) {
+              if (DIAG_ != 3) {
                 if constexpr (CG == 2) tc::mma_f16_pair(tmem + slot * BN, ad, bd, idesc, acc);
                 else tc::mma_f16(tmem + slot * BN, ad, bd, idesc, acc);
               }
@@ -508,7 +527,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       }
     };
     auto load = [&](int m_blk, int kb, Pre& P) {
-      if (a.diag == 1) {
+      if (DIAG_ == 1) {
 #pragma unroll
         for (int h = 0; h < kUPW; ++h) {
           P.v[h] = make_uint4(lane * 0x01010101u, kb, m_blk, 7u);
@@ -585,8 +604,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       const Seg sg = plan.get(si);
       total += sg.kb1 - sg.kb0;
     }
+    const int per = a.n_kblk, wb = (int)blockIdx.x / CG, wg = (int)gridDim.x / CG;
     struct Cursor {
-      int si, m_blk, kb, kb1;
+      int si, m_blk, kb, kb1;  // segment (stream-K) or tile (whole tiles), m-block, k-block, end
     };
     auto set_seg = [&](Cursor& c) {
       if (c.si < plan.nseg) {
@@ -597,13 +617,26 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       }
     };
     auto advance = [&](Cursor& c) {
-      if (++c.kb == c.kb1) {
-        ++c.si;
-        set_seg(c);
+      if constexpr (!SKT) {
+        if (++c.kb == per) {
+          c.kb = 0;
+          c.si += wg;
+          if (c.si < ntiles) c.m_blk = item(c.si).m_blk;  // once per tile
+        }
+      } else {
+        if (++c.kb == c.kb1) {
+          ++c.si;
+          set_seg(c);
+        }
       }
     };
     Cursor cl{0, 0, 0, 0};  // load cursor (2 ahead)
-    set_seg(cl);
+    if constexpr (!SKT) {
+      cl.si = wb;
+      cl.m_blk = wb < ntiles ? item(wb).m_blk : 0;
+    } else {
+      set_seg(cl);
+    }
     Cursor cp = cl;                                              // process cursor
     auto coords = [&](int, int& m_blk, int& kb) {  // next position of the load cursor
       m_blk = cl.m_blk;
@@ -631,7 +664,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       advance(cp);
       const int s = it % kStagesA;
       mbar_wait(&emptyA[s], ((it / kStagesA) & 1) ^ 1);
-      if (a.diag != 2 && a.diag != 5) process(mb, kb, P0, sA + s * kStageA);
+      if (DIAG_ != 2 && DIAG_ != 5) process(mb, kb, P0, sA + s * kStageA);
       if (tr && pw == 0 && lane == 0 && it == 0) stamp(6);
       P0 = P1;
       P1 = P2;
@@ -660,7 +693,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     const int pb = plan.b;
     auto vid = [&](int pp) { return pp * CG + (int)rank; };
     int p_lo = pb;
-    const bool fixup = a.sk && sg.fin && sg.kb0 > 0;
+    const bool fixup = SKT && sg.fin && sg.kb0 > 0;
     constexpr int kCbChunk = 32 * 32 * 4;  // bytes of one warp's 32 rows x 32 columns
     uint8_t* ring = sA + ew * kRing * kCbChunk;
     int n_chunk = 0, c_use = 0;
@@ -706,7 +739,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       if (tr && ew == 0 && lane == 0 && q == 0) stamp(4);
       const int row_base = m_blk * BM + quad * 32;  // channel (fwd) / B200 column (dgrad) of lane 0
       auto body = [&](int cb, uint32_t (&r)[32]) {
-        if (a.sk && !sg.fin) {
+        if (SKT && !sg.fin) {
           float4* dst = reinterpret_cast<float4*>(a.part + (size_t)vid(pb) * (NSUB * BN * BM) +
                                                   (((size_t)(j * (BN / 32) + cb) * 4 + quad) * 1024)) + lane;
 #pragma unroll
@@ -735,7 +768,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
             }
           }
         }
-        if (a.diag == 6) return;  // profiling: TMEM loads only
+        if (DIAG_ == 6) return;  // profiling: TMEM loads only
         if (a.tma_out) {
           // [32 tokens][32 channels] block -> one TMA store (clipped at the tensor's edges)
           int col0 = row_base;
@@ -774,7 +807,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
         __syncwarp();
         // thread = one token, 32 consecutive rows
         const int tok = ti.tok0 + j * BN + cb * 32 + lane;
-        if (tok < a.T && a.diag != 7) {  // 7: profiling, no global stores
+        if (tok < a.T && DIAG_ != 7) {  // 7: profiling, no global stores
           const T* src = stg + lane * kEpiStride;
           if (MODE == MODE_FWD || a.fast_out) {
             int col0 = row_base;
@@ -803,19 +836,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
         }
         __syncwarp();
       };
-      // TMEM loads one column block ahead of the stores (BN / 32 is even)
+      // (loading the next column block ahead of the stores measured no gain and pushed the
+      // kernel past 128 registers)
       const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + acc * BN;
-      uint32_t ra[32], rb[32];
-      tc::tmem_ld32_async(tbase, ra);
-      tc::tmem_wait_ld(ra);
 #pragma unroll 1
-      for (int cb = 0; cb < BN / 32; cb += 2) {
-        tc::tmem_ld32_async(tbase + (cb + 1) * 32, rb);
-        body(cb, ra);
-        tc::tmem_wait_ld(rb);
-        if (cb + 2 < BN / 32) tc::tmem_ld32_async(tbase + (cb + 2) * 32, ra);
-        body(cb + 1, rb);
-        if (cb + 2 < BN / 32) tc::tmem_wait_ld(ra);
+      for (int cb = 0; cb < BN / 32; ++cb) {
+        uint32_t r[32];
+        tc::tmem_ld32(tbase + cb * 32, r);
+        body(cb, r);
       }
       tc::fence_before();
       __syncwarp();
@@ -824,13 +852,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
         else mbar_arrive(&tempty_bar[acc]);
       }
     }
-    if (a.sk && !sg.fin) {
+    if (SKT && !sg.fin) {
       // publish this CTA's partial: every writer fences, then one release store
       __threadfence();
       named_bar_sync(1, kEpiWarps * 32);
       if (ew == 0 && lane == 0)
         asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(a.flags + vid(pb)), "r"(1) : "memory");
-    } else if (a.sk && sg.fin && sg.kb0 > 0) {
+    } else if (SKT && sg.fin && sg.kb0 > 0) {
       // every epilogue warp is done reading the partials: re-arm the producers' flags
       named_bar_sync(1, kEpiWarps * 32);
       if (ew == 0 && lane == 0)
@@ -1169,10 +1197,12 @@ int launch_gemm(const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap&
   static_assert(Sh::kSmem <= 227 * 1024, "GEMM smem");
   static_assert(kEpiWarps * kRing * 4096 <= Sh::kStagesA * kStageA + Sh::kStagesB * Sh::kStageB,
                 "stream-K fix-up ring fits the stage memory");
-  auto kern = gemm_kernel<MODE, BITS, T, BN, NSUB, CG>;
+  auto kern_dp = gemm_kernel<MODE, BITS, T, BN, NSUB, CG, false>;
+  auto kern_sk = gemm_kernel<MODE, BITS, T, BN, NSUB, CG, true>;
   static bool attr = false;
   if (!attr) {
-    QEFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    QEFT_CUDA(cudaFuncSetAttribute(kern_dp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    QEFT_CUDA(cudaFuncSetAttribute(kern_sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   GemmArgs b = a;
@@ -1212,6 +1242,7 @@ int launch_gemm(const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap&
     }
   }
   const int grid = CG * (b.sk ? workers : std::min(b.n_items, workers));
+  auto kern = b.sk ? kern_sk : kern_dp;
   if (CG == 2) {
     QEFT_CUDA(launch_pdl_cluster(kern, dim3(grid), dim3(kThreads), smem, st, 2, m0, m1, mw, my, b));
   } else {

@@ -124,7 +124,7 @@ QEFT_DEV uint2 lds64(const void* p) { return *reinterpret_cast<const uint2*>(p);
 // Launch shape (template): NW warps per CTA, CPS 128-column chunks per codes stage (a stage
 // holds CPS KB of 4-bit codes + their sz16 pairs, or CPS / 2 weak tiles), R stages per ring.
 // ONE: a single activation column (batch-1 decode): only column 0 of the MMA output is live.
-template <int BITS, int NT, int GT, typename T, int R, int NW, int CPS, bool ONE, int MINB, int PRE>
+template <int BITS, int NT, int GT, typename T, int R, int NW, int CPS, bool ONE, int MINB, int PRE, bool CONTIG>
 __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
   constexpr int kWPS = CPS / 2;
   constexpr int kSzOff = CPS * 1024, kStage = CPS * 1152;  // codes, then sz16 pairs
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
   uint8_t* ring = smem + (size_t)warp * R * kStage;
   float* red = reinterpret_cast<float*>(smem + (size_t)NW * R * kStage);
   const int redn = 16 * n;  // floats per (row-block, warp)
-  T* xs = reinterpret_cast<T*>(red + (size_t)(a.contig ? a.J + NW : a.J * NW) * redn);
+  T* xs = reinterpret_cast<T*>(red + (size_t)(CONTIG ? a.J + NW : a.J * NW) * redn);
   float* xsum = reinterpret_cast<float*>(xs + (size_t)n * a.xs_ld);
 
   // this CTA: row-blocks [j0, j0 + nj) of the cluster, K slice `rank`; stages of row-block jl
@@ -156,11 +156,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
   const int j0 = clu * a.J, nj = max(min(a.J, a.n_rb - j0), 0);
   const int ncs = sg.ncs, nst = sg.nst;
   const int total = nj * nst;
-  const int s_beg = a.contig ? run_start(warp, total, NW) : warp;
-  const int my_n = a.contig ? run_start(warp + 1, total, NW) - s_beg
+  const int s_beg = CONTIG ? run_start(warp, total, NW) : warp;
+  const int my_n = CONTIG ? run_start(warp + 1, total, NW) - s_beg
                             : (warp < total ? (total - warp + NW - 1) / NW : 0);
-  const int sstep = a.contig ? 1 : NW;
-  const int nslot = a.contig ? nj + NW : nj * NW;  // partial slots (redn floats each)
+  const int sstep = CONTIG ? 1 : NW;
+  const int nslot = CONTIG ? nj + NW : nj * NW;  // partial slots (redn floats each)
 
   // ---- lane 0: bulk-copy issue (stage i of this warp = global stage warp + i * NW) ----
   int issued = 0;
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
     for (int q = 0; q < NG; ++q) fold(st + kSzOff + q * 64, ga + q, d[q]);
   };
   auto park = [&](int jl) {  // this warp's partial of row-block jl -> shared memory
-    float* rp = red + (size_t)(a.contig ? jl + warp : jl * NW + warp) * redn;
+    float* rp = red + (size_t)(CONTIG ? jl + warp : jl * NW + warp) * redn;
     if constexpr (ONE) {
       if (t4 == 0) {
         rp[g8] = acc[0][0];
@@ -523,11 +523,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
   // ---- this CTA's slice partial of every row-block: sum the warps in order (into the slot
   // of the first contributing warp: fslot) ----
   auto fslot = [&](int jq, int nst_r) {
-    return a.contig ? jq + warp_of_stage(jq * nst_r, nj * nst_r, NW) : jq * NW;
+    return CONTIG ? jq + warp_of_stage(jq * nst_r, nj * nst_r, NW) : jq * NW;
   };
   for (int e = threadIdx.x; e < nj * redn; e += NW * 32) {
     const int jq = e / redn, r = e - jq * redn;
-    if (a.contig) {
+    if (CONTIG) {
       const int wa = warp_of_stage(jq * nst, total, NW), wb = warp_of_stage(jq * nst + nst - 1, total, NW);
       float* p = red + (size_t)jq * redn + r;
       float v = 0.f;
@@ -620,13 +620,15 @@ SliceGeo slice_geo(const Geom& G, int u0, int u1) {
 
 // MINB CTAs per SM (2: a CTA of the next launch can start -- and prefetch its weights --
 // beside a CTA of this one)
-template <int BITS, int NT, int GT, typename T, int R, int NW, int CPS, int MINB = 1, int GPS = MINB>
+template <int BITS, int NT, int GT, typename T, int R, int NW, int CPS, bool CONTIG = false, int MINB = 1,
+          int GPS = MINB>
 int launch2(G2Args a, cudaStream_t st) {
+  a.contig = CONTIG;
   constexpr int kStage = CPS * 1152;
   constexpr int kSmemMax = (MINB == 1 ? 227 * 1024 : 113 * 1024) - 1024;
   constexpr int PRE = MINB > 1 ? R : 0;  // pre-wait weight prefetch only when CTAs can overlap
-  auto kern1 = gemv2_kernel<BITS, NT, GT, T, R, NW, CPS, true, MINB, PRE>;
-  auto kernN = gemv2_kernel<BITS, NT, GT, T, R, NW, CPS, false, MINB, PRE>;
+  auto kern1 = gemv2_kernel<BITS, NT, GT, T, R, NW, CPS, true, MINB, PRE, CONTIG>;
+  auto kernN = gemv2_kernel<BITS, NT, GT, T, R, NW, CPS, false, MINB, PRE, CONTIG>;
   const bool one = a.n == 1 && NT == 1;
   auto kern = one ? kern1 : kernN;
   static bool attr = false;
@@ -746,45 +748,43 @@ int dispatch2(const G2Args& a, int gt, cudaStream_t st) {
         case 1: return launch2<4, 1, 2, T, 3, 8, 4>(a, st);
         case 2: return launch2<4, 1, 2, T, 2, 8, 8>(a, st);
         case 3: return launch2<4, 1, 2, T, 2, 12, 4>(a, st);
-        case 4: return launch2<4, 1, 2, T, 2, 8, 4, 2>(a, st);
-        case 5: return launch2<4, 1, 2, T, 2, 16, 4, 1>(a, st);
-        case 6: return launch2<4, 1, 2, T, 2, 8, 4, 2, 1>(a, st);
+        case 4: return launch2<4, 1, 2, T, 2, 8, 4, false, 2>(a, st);
+        case 5: return launch2<4, 1, 2, T, 2, 16, 4, false, 1>(a, st);
+        case 6: return launch2<4, 1, 2, T, 2, 8, 4, false, 2, 1>(a, st);
         default: break;
       }
     }
   }
   // launch2 returns -1 when the plan does not fit shared memory: try the next shape
-#define QEFT_G2(CONTIG, NT, NWV, CPSV)                                           \
-  {                                                                              \
-    G2Args b_ = a;                                                               \
-    b_.contig = CONTIG;                                                          \
-    int r_ = -1;                                                                 \
-    switch (gt) {                                                                \
-      case 1: r_ = launch2<BITS, NT, 1, T, 2, NWV, CPSV>(b_, st); break;         \
-      case 2: r_ = launch2<BITS, NT, 2, T, 2, NWV, CPSV>(b_, st); break;         \
-      case 4: r_ = launch2<BITS, NT, 4, T, 2, NWV, CPSV>(b_, st); break;         \
-      default: if constexpr (CPSV >= 4) r_ = launch2<BITS, NT, 8, T, 2, NWV, (CPSV >= 4 ? CPSV : 4)>(b_, st); break; \
-    }                                                                            \
-    if (r_ != -1) return r_;                                                     \
+#define QEFT_G2(CONTIG, NT, NWV, CPSV)                                                   \
+  {                                                                                      \
+    int r_ = -1;                                                                         \
+    switch (gt) {                                                                        \
+      case 1: r_ = launch2<BITS, NT, 1, T, 2, NWV, CPSV, CONTIG>(a, st); break;          \
+      case 2: r_ = launch2<BITS, NT, 2, T, 2, NWV, CPSV, CONTIG>(a, st); break;          \
+      case 4: r_ = launch2<BITS, NT, 4, T, 2, NWV, CPSV, CONTIG>(a, st); break;          \
+      default: if constexpr (CPSV >= 4) r_ = launch2<BITS, NT, 8, T, 2, NWV, (CPSV >= 4 ? CPSV : 4), CONTIG>(a, st); break; \
+    }                                                                                    \
+    if (r_ != -1) return r_;                                                             \
   }
   // 16 warps whenever the partials and the staged x fit (the decode + MMA issue rate is the
   // limit). Round-robin stage dealing streams neighbouring stages from all warps at once
   // (measured 3.5 % faster at n = 1) but needs J x NW partial slots; contiguous runs need
   // J + NW, so up to 8 columns fit beside 16 rings (n = 4: +31 %, n = 8: +26 %,
   // profiles/r02/batch_ab.json). 16 columns stage 16 rows of x and may need 2 KB stages or 8 warps.
-  const int cmode = a.contig;  // QEFT_GEMV2_CONTIG: 0 never, 1 when it enables more warps, 2 always
+  const int cmode = a.contig;  // QEFT_GEMV2_CONTIG: 0 never, 1 when it enables more warps
   if (nt2) {
-    if (cmode) QEFT_G2(1, 2, 16, 4)
-    if (cmode) QEFT_G2(1, 2, 16, 2)
-    if (cmode) QEFT_G2(1, 2, 8, 4)
-    if (cmode && gt <= 4) QEFT_G2(1, 2, 8, 2)
-    QEFT_G2(0, 2, 8, 4)
+    if (cmode) QEFT_G2(true, 2, 16, 4)
+    if (cmode) QEFT_G2(true, 2, 16, 2)
+    if (cmode) QEFT_G2(true, 2, 8, 4)
+    if (cmode && gt <= 4) QEFT_G2(true, 2, 8, 2)
+    QEFT_G2(false, 2, 8, 4)
   } else if (a.n > 2) {
-    if (cmode != 2) QEFT_G2(0, 1, 16, 4)
-    if (cmode) QEFT_G2(1, 1, 16, 4)
-    QEFT_G2(cmode == 2, 1, 8, 4)
+    QEFT_G2(false, 1, 16, 4)
+    if (cmode) QEFT_G2(true, 1, 16, 4)
+    QEFT_G2(false, 1, 8, 4)
   } else {
-    QEFT_G2(cmode == 2, 1, 16, 4)
+    QEFT_G2(false, 1, 16, 4)
   }
   return -1;
 #undef QEFT_G2

@@ -17,6 +17,8 @@ is refreshed from the master after each optimizer step.
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import _lib
@@ -57,13 +59,16 @@ class _QEFTLinearFn(torch.autograd.Function):
         return dx, None, None, None
 
 
+_WEAK_VIEW = os.environ.get("QEFT_WEAK_VIEW", "1") != "0"  # A/B knob: 0 = always gather
+
+
 def _weak_slice(dl: DeviceLayer, x2):
     """x_weak for the backward (TrainableLayerState.x_weak, tuning.py:30-34, 70-71). Structured
     layers hold their weak block in the trailing input columns [m, ic): the wgrad GEMM reads
     that strided view of x in place by TMA (row pitch ic), so no copy is made and no kernel
     launched -- the role the GEMM epilogue would otherwise play. Other layouts gather the k
     weak columns (one small launch)."""
-    if (dl.structured_fast and x2.stride(1) == 1 and x2.stride(0) % 8 == 0 and dl.m % 8 == 0
+    if (_WEAK_VIEW and dl.structured_fast and x2.stride(1) == 1 and x2.stride(0) % 8 == 0 and dl.m % 8 == 0
             and x2.data_ptr() % 16 == 0 and x2.shape[0] > 1):
         return x2[:, dl.m:dl.m + dl.k]
     return dl.gather_weak(x2)

@@ -1,0 +1,12 @@
+O=gpurun_out/c41; mkdir -p $O
+old() { (cd _ab_old && timeout 600 python bench.py --no-cpu --no-dstep --no-sweep > ../$O/old.json 2>../$O/old.err); python -c "
+import json; d=json.load(open('$O/old.json')); ft=d['finetune']; print('OLD r02', round(ft['value']), round(ft['ms_per_step'],2))"; }
+run() { env "$@" timeout 600 python bench.py --no-cpu --no-dstep --no-sweep > $O/b.json 2>$O/b.err; python -c "
+import json; d=json.load(open('$O/b.json')); ft=d['finetune']; print('$*', round(ft['value']), round(ft['ms_per_step'],2))"; }
+old
+run X=1
+run QEFT_GEMM_SK=0
+run QEFT_GEMM_TMA_OUT=0
+run QEFT_WEAK_VIEW=0
+run QEFT_GEMM_SK=0 QEFT_WEAK_VIEW=0
+old
