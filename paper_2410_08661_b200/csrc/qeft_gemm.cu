@@ -347,6 +347,42 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     return it;
   };
 
+  // [32 tokens][32 channels] block of the accumulator (thread = channel row, r = its 32 token
+  // columns) -> fp16/bf16 staging `buf` -> one TMA store (clipped at the tensor's edges;
+  // reduce-add when accumulating). row_base: the block's first row (channel / B200 column).
+  auto tma_block = [&](const uint32_t (&r)[32], int row_base, int tc0, T* buf) {
+    int col0 = row_base;
+    bool ok = true;
+    if (MODE == MODE_FWD) {
+      ok = row_base < a.oc;
+    } else if (row_base < a.m_pad) {
+      ok = row_base < a.m;  // [m, m_pad) is padding: its columns belong to the weak block
+    } else {
+      col0 = a.m + (row_base - a.m_pad);
+      ok = row_base - a.m_pad < a.k;
+    }
+    ok = ok && tc0 < a.T;
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");  // buffer free
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < 32; ++c) buf[c * 32 + lane] = from_f32<T>(__uint_as_float(r[c]));
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0 && ok) {
+      if (a.accumulate)
+        asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];\n"
+                     ::"l"(&map_y), "r"(col0), "r"(tc0), "r"(smem_u32(buf)) : "memory");
+      else
+        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];\n"
+                     ::"l"(&map_y), "r"(col0), "r"(tc0), "r"(smem_u32(buf)) : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
+  };
+  // whole-tile kernels: the producer warps, idle once their last k-block is dequantized, drain
+  // two thirds of the CTA's LAST tile (its column blocks u = j * BN / 32 + cb with u % 3 != 0)
+  // beside the epilogue warps -- that tile's epilogue is nobody else's overlap
+  const bool join = !SKT && a.tma_out;
+
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStagesA; ++s) {
       mbar_init(&fullA[s], 1 + CG * kProdWarps);  // leader's TMA warp (weak bytes, maybe 0) + producers
@@ -675,6 +711,33 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
         else mbar_arrive(&fullA[s]);
       }
     }
+    if (join && plan.nseg > 0) {
+      int q_last = 0;  // the epilogue's sub-tile counter at the CTA's last tile
+      for (int si = 0; si + 1 < plan.nseg; ++si) q_last += item(plan.get(si).tile).nsub;
+      const Item ti = item(plan.get(plan.nseg - 1).tile);
+      // every MMA of the tile is done (so the A stages are free staging) once its last
+      // sub-tile's accumulator is full
+      const int ql = q_last + ti.nsub - 1;
+      mbar_wait(&tfull_bar[ql & 1], (ql >> 1) & 1);
+      tc::fence_after();
+      const int quad = warp & 3, role = 1 + (pw >> 2);  // epilogue warp of this quadrant: role 0
+      T* pbuf = reinterpret_cast<T*>(sA) + (size_t)pw * 2048;
+      int nb = 0;
+      for (int j = 0; j < ti.nsub; ++j) {
+        const int qq = q_last + j;
+        mbar_wait(&tfull_bar[qq & 1], (qq >> 1) & 1);
+        tc::fence_after();
+        const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + (qq & 1) * BN;
+#pragma unroll 1
+        for (int cb = 0; cb < BN / 32; ++cb) {
+          if ((j * (BN / 32) + cb) % 3 != role) continue;
+          uint32_t r[32];
+          tc::tmem_ld32(tbase + cb * 32, r);
+          tma_block(r, ti.m_blk * BM + quad * 32, ti.tok0 + j * BN + cb * 32, pbuf + (nb++ & 1) * 1024);
+        }
+      }
+      tc::fence_before();
+    }
   } else {
     // ================= epilogue: TMEM -> registers -> smem transpose -> global =================
     const int ew = warp - (2 + kProdWarps);
@@ -770,35 +833,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
         }
         if (DIAG_ == 6) return;  // profiling: TMEM loads only
         if (a.tma_out) {
-          // [32 tokens][32 channels] block -> one TMA store (clipped at the tensor's edges)
-          int col0 = row_base;
-          bool ok = true;
-          if (MODE == MODE_FWD) {
-            ok = row_base < a.oc;
-          } else if (row_base < a.m_pad) {
-            ok = row_base < a.m;  // [m, m_pad) is padding: its columns belong to the weak block
-          } else {
-            col0 = a.m + (row_base - a.m_pad);
-            ok = row_base - a.m_pad < a.k;
-          }
-          const int tc0 = ti.tok0 + j * BN + cb * 32;
-          ok = ok && tc0 < a.T;
-          T* buf = sE + (size_t)ew * 2048 + (cb & 1) * 1024;
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");  // buffer free
-          __syncwarp();
-#pragma unroll
-          for (int c = 0; c < 32; ++c) buf[c * 32 + lane] = from_f32<T>(__uint_as_float(r[c]));
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0 && ok) {
-            if (a.accumulate)
-              asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];\n"
-                           ::"l"(&map_y), "r"(col0), "r"(tc0), "r"(smem_u32(buf)) : "memory");
-            else
-              asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];\n"
-                           ::"l"(&map_y), "r"(col0), "r"(tc0), "r"(smem_u32(buf)) : "memory");
-            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-          }
+          tma_block(r, row_base, ti.tok0 + j * BN + cb * 32, sE + (size_t)ew * 2048 + (cb & 1) * 1024);
           return;
         }
         // thread = one row (channel), 32 token columns -> staging [token][row]
@@ -839,8 +874,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       // (loading the next column block ahead of the stores measured no gain and pushed the
       // kernel past 128 registers)
       const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + acc * BN;
+      const bool shared_drain = join && si == plan.nseg - 1;  // producers take u % 3 != 0
 #pragma unroll 1
       for (int cb = 0; cb < BN / 32; ++cb) {
+        if (shared_drain && (j * (BN / 32) + cb) % 3 != 0) continue;
         uint32_t r[32];
         tc::tmem_ld32(tbase + cb * 32, r);
         body(cb, r);
@@ -867,7 +904,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     }
   }
 
-  if (warp >= 2 + kProdWarps && lane == 0 && a.tma_out)
+  if (warp >= 2 && lane == 0 && a.tma_out)
     asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // output stores done before exit
   if (tr && warp == 2 + kProdWarps && lane == 0) stamp(5);
   __syncthreads();
