@@ -226,6 +226,16 @@ int qeft_silu_mul_fwd(const void* g, const void* u, void* f, int64_t n, int dt, 
 int qeft_silu_mul_bwd(const void* df, const void* g, const void* u, void* dg, void* du, int64_t n, int dt,
                       void* stream);
 
+/* Next-token cross-entropy over fp16/bf16 logits z [rows][ldz] (V classes, V and the row
+ * pitches multiples of 8, V <= 65536), fp32 math (model.py:531-547):
+ * fwd: loss[r] = lse[r] - z[r][tgt[r]], lse[r] = log(sum_v exp(z[r][v])) (saved for bwd);
+ * bwd: dz[r][v] = (exp(z[r][v] - lse[r]) - [v == tgt[r]]) * (*gscale), in z's dtype
+ *      (gscale: device fp32, e.g. dL/dmean / rows). */
+int qeft_cross_entropy_fwd(const void* z, int64_t ldz, int rows, int V, const int64_t* tgt, float* loss,
+                           float* lse, int dt, void* stream);
+int qeft_cross_entropy_bwd(const void* z, int64_t ldz, int rows, int V, const int64_t* tgt, const float* lse,
+                           const float* gscale, void* dz, int64_t lddz, int dt, void* stream);
+
 /* Thread-local message for the last non-zero return. */
 const char* qeft_last_error(void);
 /* Library build string (arch, version). */

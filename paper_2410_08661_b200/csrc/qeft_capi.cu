@@ -197,6 +197,16 @@ int qeft_rope(const void* in, void* out, const float* cosv, const float* sinv, i
   return rope(in, out, cosv, sinv, rows, T, H, hd, inverse, dt, ST(s));
 }
 
+int qeft_cross_entropy_fwd(const void* z, int64_t ldz, int rows, int V, const int64_t* tgt, float* loss,
+                           float* lse, int dt, void* s) {
+  return cross_entropy_fwd(z, ldz, rows, V, tgt, loss, lse, dt, ST(s));
+}
+
+int qeft_cross_entropy_bwd(const void* z, int64_t ldz, int rows, int V, const int64_t* tgt, const float* lse,
+                           const float* gscale, void* dz, int64_t lddz, int dt, void* s) {
+  return cross_entropy_bwd(z, ldz, rows, V, tgt, lse, gscale, dz, lddz, dt, ST(s));
+}
+
 int qeft_silu_mul_fwd(const void* g, const void* u, void* f, int64_t n, int dt, void* s) {
   return silu_mul_fwd(g, u, f, n, dt, ST(s));
 }

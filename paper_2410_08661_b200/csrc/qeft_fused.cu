@@ -227,6 +227,94 @@ __global__ void silu_mul_bwd_kernel(const T* __restrict__ df, const T* __restric
   }
 }
 
+// Next-token cross-entropy over fp16/bf16 logits (the reference's fp32 log-softmax NLL,
+// model.py:531-547): one CTA per row, the row read once into registers (16-byte vectors), fp32
+// max / sum of exp by block reduction in a fixed order (deterministic), loss[row] = lse - z_t.
+// The backward recomputes exp(z - lse) from the logits and the saved lse:
+// dz = (softmax - onehot(t)) * g, written in the logits' dtype, g = dL/dloss / rows (device).
+constexpr int kCeThreads = 512, kCeVec = 8;
+
+template <int NT>
+__device__ __forceinline__ float block_reduce(float v, float* sh, bool is_max) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const float w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmaxf(v, w) : v + w;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();  // sh reuse across calls
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  v = lane < NT / 32 ? sh[lane] : (is_max ? -INFINITY : 0.f);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const float w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmaxf(v, w) : v + w;
+  }
+  return v;
+}
+
+template <typename T, int PER>
+__global__ void __launch_bounds__(kCeThreads) ce_fwd_kernel(const T* __restrict__ z, int64_t ldz, int V,
+                                                            const int64_t* __restrict__ tgt, float* __restrict__ loss,
+                                                            float* __restrict__ lse_out) {
+  __shared__ float sh[32];
+  const T* row = z + (int64_t)blockIdx.x * ldz;
+  const int nv = V / kCeVec;
+  uint4 v[PER];
+  float m = -INFINITY;
+#pragma unroll
+  for (int p = 0; p < PER; ++p) {
+    const int i = threadIdx.x + p * kCeThreads;
+    if (i < nv) {
+      v[p] = *reinterpret_cast<const uint4*>(row + (int64_t)i * kCeVec);
+      const T* e = reinterpret_cast<const T*>(&v[p]);
+#pragma unroll
+      for (int k = 0; k < kCeVec; ++k) m = fmaxf(m, to_f32<T>(e[k]));
+    }
+  }
+  m = block_reduce<kCeThreads>(m, sh, true);
+  float s = 0.f;
+#pragma unroll
+  for (int p = 0; p < PER; ++p) {
+    const int i = threadIdx.x + p * kCeThreads;
+    if (i < nv) {
+      const T* e = reinterpret_cast<const T*>(&v[p]);
+#pragma unroll
+      for (int k = 0; k < kCeVec; ++k) s += __expf(to_f32<T>(e[k]) - m);
+    }
+  }
+  s = block_reduce<kCeThreads>(s, sh, false);
+  if (threadIdx.x == 0) {
+    const float lse = m + __logf(s);
+    lse_out[blockIdx.x] = lse;
+    loss[blockIdx.x] = lse - to_f32<T>(row[tgt[blockIdx.x]]);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) ce_bwd_kernel(const T* __restrict__ z, int64_t ldz, int V,
+                                                     const int64_t* __restrict__ tgt, const float* __restrict__ lse,
+                                                     const float* __restrict__ gscale, T* __restrict__ dz,
+                                                     int64_t lddz) {
+  const T* row = z + (int64_t)blockIdx.y * ldz;
+  T* drow = dz + (int64_t)blockIdx.y * lddz;
+  const float l = lse[blockIdx.y], g = *gscale;
+  const int t = (int)tgt[blockIdx.y];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < V / kCeVec; i += gridDim.x * blockDim.x) {
+    const uint4 v = *reinterpret_cast<const uint4*>(row + (int64_t)i * kCeVec);
+    const T* e = reinterpret_cast<const T*>(&v);
+    uint4 o;
+    T* oe = reinterpret_cast<T*>(&o);
+#pragma unroll
+    for (int k = 0; k < kCeVec; ++k) {
+      const float p = __expf(to_f32<T>(e[k]) - l) - (i * kCeVec + k == t ? 1.f : 0.f);
+      oe[k] = from_f32<T>(p * g);
+    }
+    *reinterpret_cast<uint4*>(drow + (int64_t)i * kCeVec) = o;
+  }
+}
+
 int grid_for(int64_t n, int per_thread) {
   const int64_t blocks = (n / per_thread + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 16));
@@ -299,6 +387,43 @@ int rope(const void* in, void* out, const float* cosv, const float* sinv, int64_
     if (vec) go(__half{}, std::integral_constant<int, 8>{});
     else go(__half{}, std::integral_constant<int, 1>{});
   }
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int cross_entropy_fwd(const void* z, int64_t ldz, int rows, int V, const int64_t* tgt, float* loss, float* lse,
+                      int dt, cudaStream_t st) {
+  QEFT_CHECK(V % kCeVec == 0 && ldz % kCeVec == 0 && V > 0 && rows >= 0, QEFT_ERR_SHAPE,
+             "cross_entropy: V=%d and ld=%lld must be multiples of 8", V, (long long)ldz);
+  QEFT_CHECK(V <= 16 * kCeThreads * kCeVec, QEFT_ERR_SHAPE, "cross_entropy: V=%d > %d", V, 16 * kCeThreads * kCeVec);
+  if (!rows) return 0;
+  const int per = (V / kCeVec + kCeThreads - 1) / kCeThreads;
+  auto go = [&](auto tag, auto perc) {
+    using T = decltype(tag);
+    ce_fwd_kernel<T, decltype(perc)::value><<<rows, kCeThreads, 0, st>>>((const T*)z, ldz, V, tgt, loss, lse);
+  };
+#define QEFT_CE(P)                                                                              \
+  if (per <= P) {                                                                               \
+    if (dt == QEFT_BF16) go(__nv_bfloat16{}, std::integral_constant<int, P>{});                 \
+    else go(__half{}, std::integral_constant<int, P>{});                                        \
+  } else
+  QEFT_CE(2) QEFT_CE(4) QEFT_CE(8) QEFT_CE(16) {}
+#undef QEFT_CE
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int cross_entropy_bwd(const void* z, int64_t ldz, int rows, int V, const int64_t* tgt, const float* lse,
+                      const float* gscale, void* dz, int64_t lddz, int dt, cudaStream_t st) {
+  QEFT_CHECK(V % kCeVec == 0 && ldz % kCeVec == 0 && lddz % kCeVec == 0 && V > 0, QEFT_ERR_SHAPE,
+             "cross_entropy_bwd: V=%d and lds must be multiples of 8", V);
+  if (!rows) return 0;
+  const dim3 grid((V / kCeVec + 255) / 256, rows);
+  if (dt == QEFT_BF16)
+    ce_bwd_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)z, ldz, V, tgt, lse, gscale,
+                                                       (__nv_bfloat16*)dz, lddz);
+  else
+    ce_bwd_kernel<__half><<<grid, 256, 0, st>>>((const __half*)z, ldz, V, tgt, lse, gscale, (__half*)dz, lddz);
   QEFT_CUDA(cudaGetLastError());
   return 0;
 }

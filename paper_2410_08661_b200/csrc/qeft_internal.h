@@ -66,6 +66,10 @@ int gemv2_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t l
 
 size_t gemm_workspace_bytes(const qeft_linear_t* L, int T);
 int gemm_set_schedule(int what, int value);
+int cross_entropy_fwd(const void* z, int64_t ldz, int rows, int V, const int64_t* tgt, float* loss, float* lse,
+                      int dt, cudaStream_t st);
+int cross_entropy_bwd(const void* z, int64_t ldz, int rows, int V, const int64_t* tgt, const float* lse,
+                      const float* gscale, void* dz, int64_t lddz, int dt, cudaStream_t st);
 int gemm_fwd(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ldy, int T,
              void* ws, size_t ws_bytes, cudaStream_t st);
 int gemm_dgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, void* dx, int64_t lddx, int T,

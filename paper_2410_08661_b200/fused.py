@@ -87,6 +87,40 @@ class _SiluMul(torch.autograd.Function):
         return dg, du
 
 
+class _CrossEntropy(torch.autograd.Function):
+    """Mean next-token NLL of fp16/bf16 logits (rows, V) in fp32 math, no fp32 copy of the
+    logits: qeft_cross_entropy_fwd keeps lse per row; the backward recomputes the softmax."""
+
+    @staticmethod
+    def forward(ctx, z, tgt):
+        rows, V = z.shape
+        zc = z if z.stride(1) == 1 and z.stride(0) % 8 == 0 and z.data_ptr() % 16 == 0 else z.contiguous()
+        t = tgt.contiguous().to(torch.int64)
+        loss = torch.empty(rows, dtype=torch.float32, device=z.device)
+        lse = torch.empty(rows, dtype=torch.float32, device=z.device)
+        _lib.check(_lib.lib().qeft_cross_entropy_fwd(zc.data_ptr(), zc.stride(0), rows, V, t.data_ptr(),
+                                                     loss.data_ptr(), lse.data_ptr(), _TDT[z.dtype],
+                                                     _lib.stream_ptr()), "cross_entropy_fwd")
+        ctx.save_for_backward(zc, t, lse)
+        return loss.mean()
+
+    @staticmethod
+    def backward(ctx, g):
+        zc, t, lse = ctx.saved_tensors
+        rows, V = zc.shape
+        gs = (g.float() / rows).reshape(1).contiguous()
+        dz = torch.empty_like(zc)
+        _lib.check(_lib.lib().qeft_cross_entropy_bwd(zc.data_ptr(), zc.stride(0), rows, V, t.data_ptr(),
+                                                     lse.data_ptr(), gs.data_ptr(), dz.data_ptr(), dz.stride(0),
+                                                     _TDT[zc.dtype], _lib.stream_ptr()), "cross_entropy_bwd")
+        return dz, None
+
+
+def cross_entropy(z, tgt):
+    """mean_r(logsumexp(z[r]) - z[r, tgt[r]]) for fp16/bf16 CUDA logits (rows, V)."""
+    return _CrossEntropy.apply(z, tgt)
+
+
 def rms_norm(x, gain):
     return _RMSNorm.apply(x, gain)
 

@@ -181,6 +181,9 @@ class QEFTDecoder(torch.nn.Module):
 
 
 def cross_entropy_mean(logits, targets):
-    """Mean next-token NLL over all positions (model.py:531-547), fp32 softmax."""
+    """Mean next-token NLL over all positions (model.py:531-547), fp32 softmax. fp16/bf16 CUDA
+    logits take the fused kernel (no fp32 copy of the (tokens x vocab) logits)."""
     V = logits.shape[-1]
+    if fused.supported(logits) and V % 8 == 0 and V <= 65536:
+        return fused.cross_entropy(logits.reshape(-1, V), targets.reshape(-1))
     return F.cross_entropy(logits.float().reshape(-1, V), targets.reshape(-1), reduction="mean")

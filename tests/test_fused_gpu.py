@@ -100,3 +100,28 @@ def test_block_fused_matches_torch_path(torch_):
     finally:
         fused.supported = orig
     assert rel_err(_np(y_f), _np(y_t)) <= 2e-2
+
+
+@pytest.mark.parametrize("dt,rows,V", [("f16", 64, 32000), ("bf16", 33, 1000), ("f16", 5, 8)])
+def test_cross_entropy_matches_fp32_torch(dt, rows, V):
+    """Fused CE (qeft_cross_entropy_fwd/bwd) against F.cross_entropy on the fp32 image of the
+    same logits (the reference's fp32 log-softmax NLL, model.py:531-547): loss to 1e-5
+    relative, gradient to one output rounding of the logits' dtype."""
+    import torch
+    import torch.nn.functional as F
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2410_08661_b200 import fused
+    td = torch.float16 if dt == "f16" else torch.bfloat16
+    g = torch.Generator(device="cuda").manual_seed(rows + V)
+    z = (torch.randn(rows, V, device="cuda", generator=g) * 3).to(td).requires_grad_(True)
+    t = torch.randint(0, V, (rows,), device="cuda", generator=g)
+    loss = fused.cross_entropy(z, t)
+    loss.backward(torch.tensor(1.7, device="cuda"))
+    zr = z.detach().float().requires_grad_(True)
+    ref = F.cross_entropy(zr, t, reduction="mean")
+    (ref * 1.7).backward()
+    assert abs(float(loss) - float(ref)) <= 1e-5 * abs(float(ref))
+    ulp = 2.0 ** -10 if dt == "f16" else 2.0 ** -7
+    err = (z.grad.float() - zr.grad.to(td).float()).abs().max()
+    assert float(err) <= ulp * float(zr.grad.abs().max()) + 1e-7
