@@ -9,6 +9,9 @@ timeout 1200 python -m pytest tests -m gpu -q > $O/pytest_gpu.txt 2>&1; tail -2 
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1; tail -2 $O/smoke.txt
 timeout 1200 python bench.py > $O/bench.json 2> $O/bench.err
 timeout 600 python scripts/configs_perf.py > $O/configs_perf.json 2> $O/configs_perf.err
+timeout 300 python scripts/ab_gemm.py > $O/ab_gemm.txt 2>&1
+timeout 300 python scripts/ab_gemm_cold.py > $O/ab_gemm_cold.txt 2>&1
+timeout 600 python scripts/ft_step.py --steps 5 > $O/ft_step.txt 2>&1
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 timeout 600 ncu --metrics $M --clock-control none -k regex:gemv -c 256 --csv --log-file $O/decode_launches.csv \
   python bench.py --steps 1 --warmup 3 --no-ft --no-dstep --no-sweep --no-cpu > /dev/null 2>&1
