@@ -70,6 +70,7 @@ struct GemmArgs {
   float* part;
   int* flags;
   unsigned long long* trace;  // profiling only (qeft_gemv_trace slots): per-CTA globaltimer stamps
+  int b200_out;    // dgrad: write dX in B200 K order (all m_pad + k_pad columns; a scatter follows)
   int tma_out;     // epilogue writes 32 x 32 output blocks with TMA stores (reduce-add to accumulate)
   int diag;  // profiling only (QEFT_GEMM_DIAG): 1 producers skip global loads, 2 skip dequant,
              // 3 no MMAs, 4 no activation TMA after the first ring, 5 = 2 + 4 -- results are garbage;
@@ -355,6 +356,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     bool ok = true;
     if (MODE == MODE_FWD) {
       ok = row_base < a.oc;
+    } else if (a.b200_out) {
+      ok = true;  // B200 order: the scatter drops the padding columns
     } else if (row_base < a.m_pad) {
       ok = row_base < a.m;  // [m, m_pad) is padding: its columns belong to the weak block
     } else {
@@ -1327,7 +1330,7 @@ int dispatch_gemm(const qeft_linear_t* L, int T_, const GemmPlan& p, const CUten
   static const int tma_env = getenv("QEFT_GEMM_TMA_OUT") ? atoi(getenv("QEFT_GEMM_TMA_OUT")) : 1;
   CUtensorMap my = m0;
   a.tma_out = 0;
-  if (tma_env && (MODE == MODE_FWD || a.fast_out) && (a.ldo * 2) % 16 == 0 &&
+  if (tma_env && (MODE == MODE_FWD || a.fast_out || a.b200_out) && (a.ldo * 2) % 16 == 0 &&
       ((uintptr_t)a.out & 15) == 0) {
     if (make_out_map(&my, a.out, L->act_dtype, a.out_cols, T_, a.ldo) == 0) a.tma_out = 1;
   }
@@ -1392,8 +1395,10 @@ int gemm_set_schedule(int what, int value) {
 size_t gemm_workspace_bytes(const qeft_linear_t* L, int T_) {
   // gathered activations in B200 K order (fwd, non-structured layouts), weak columns
   // (wgrad), or a 16-byte-pitched copy of dY (dgrad/wgrad when oc % 8 != 0)
-  const size_t kk = (size_t)std::max(L->m_pad + L->k_pad, pad_to(L->oc, 8) + L->k_pad);
-  return (size_t)T_ * kk * 2 + 1024;
+  // fwd: gathered x [T][m_pad + k_pad]; dgrad: pitched dY [T][pad(oc, 8)] then B200-order dX
+  // [T][m_pad + k_pad] (non-structured layouts); wgrad: x weak columns then pitched dY
+  const size_t kk = (size_t)(L->m_pad + L->k_pad);
+  return (size_t)T_ * (kk + pad_to(L->oc, 8) + L->k_pad) * 2 + 2048;
 }
 
 // dY with a row pitch TMA cannot address -> copy into ws with pitch roundup(oc, 8)
@@ -1432,7 +1437,7 @@ int gemm_fwd(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_
   } else {
     const int kk = L->m_pad + L->k_pad;
     QEFT_CHECK(ws_bytes >= (size_t)T_ * kk * 2, QEFT_ERR_SHAPE, "gemm_fwd: workspace too small");
-    if (int r = gather_cols(x, ldx, L->colmap, kk, T_, L->act_dtype, ws, st)) return r;
+    if (int r = gather_rows(x, ldx, L->ic, L->colmap, kk, T_, L->act_dtype, ws, st)) return r;
     if (int r = make_map(&m0, ws, L->act_dtype, kk, T_, kk, box)) return r;
     m1 = m0;
     a.gathered = 1;
@@ -1455,11 +1460,27 @@ int gemm_dgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, void* dx, i
   a.accumulate = accumulate;
   a.out_cols = L->ic;
   a.fast_out = (L->flags & QEFT_FLAG_STRUCTURED_FAST) && (L->m % 32 == 0);
+  // non-structured layouts (irregular W_O, online reorder): dX in B200 order into the workspace
+  // by TMA-store blocks, then one row-staged scatter through the column map (+ accumulate)
+  const int kk = L->m_pad + L->k_pad;
+  const size_t dy_bytes = (dy == ws) ? (((size_t)T_ * pad_to(L->oc, 8) * 2 + 255) & ~(size_t)255) : 0;
+  void* dxb = (char*)ws + dy_bytes;
+  const bool b200 = !a.fast_out && ws != nullptr && ws_bytes >= dy_bytes + (size_t)T_ * kk * 2 &&
+                    (((uintptr_t)dxb) & 15) == 0 && getenv("QEFT_GEMM_SCATTER_EPI") == nullptr;
+  if (b200) {
+    a.b200_out = 1;
+    a.out = dxb;
+    a.ldo = kk;
+    a.out_cols = kk;
+    a.accumulate = 0;
+  }
   CUtensorMap m0;
   const GemmPlan plan = gemm_plan(a.n_mblk, T_);
   if (int r = make_map(&m0, dy, L->act_dtype, L->oc, T_, lddy, plan.bn / plan.cg)) return r;
-  if (L->act_dtype == QEFT_F16) return dispatch_gemm<MODE_DGRAD, __half>(L, T_, plan, m0, m0, a, st);
-  return dispatch_gemm<MODE_DGRAD, __nv_bfloat16>(L, T_, plan, m0, m0, a, st);
+  int r = L->act_dtype == QEFT_F16 ? dispatch_gemm<MODE_DGRAD, __half>(L, T_, plan, m0, m0, a, st)
+                                   : dispatch_gemm<MODE_DGRAD, __nv_bfloat16>(L, T_, plan, m0, m0, a, st);
+  if (r || !b200) return r;
+  return scatter_rows(dxb, kk, L->colmap, L->ic, T_, L->act_dtype, dx, lddx, accumulate, st);
 }
 
 template <typename T, int NW>
@@ -1504,7 +1525,7 @@ int gemm_wgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, const void*
     if (int r = make_map(&mx, (const char*)x + (size_t)L->m * 2, L->act_dtype, L->k, T_, ldx, 64)) return r;
   } else {
     QEFT_CHECK(ws_bytes >= xw_bytes, QEFT_ERR_SHAPE, "gemm_wgrad: workspace too small");
-    if (int r = gather_cols(x, ldx, L->colmap + L->m_pad, L->k_pad, T_, L->act_dtype, ws, st)) return r;
+    if (int r = gather_rows(x, ldx, L->ic, L->colmap + L->m_pad, L->k_pad, T_, L->act_dtype, ws, st)) return r;
     if (int r = make_map(&mx, ws, L->act_dtype, L->k_pad, T_, L->k_pad, 64)) return r;
   }
   const int nw = L->k_pad / 64;

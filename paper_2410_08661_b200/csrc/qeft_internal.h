@@ -38,6 +38,10 @@ size_t sz16_bytes(int oc, int m, int g);
 int pack_sz16(const float* s, const float* z, int oc, int m, int g, void* out, cudaStream_t st);
 int pack_weak(const float* w, int oc, int k, int dtype, void* out, cudaStream_t st);
 int dequant_full(const qeft_linear_t* L, float* out, cudaStream_t st);
+int gather_rows(const void* x, int64_t ldx, int src_cols, const int* colmap, int kk, int rows, int dtype,
+                void* xb, cudaStream_t st);
+int scatter_rows(const void* xb, int kk, const int* colmap, int ic, int rows, int dtype, void* out, int64_t ldo,
+                 int accumulate, cudaStream_t st);
 int gather_cols(const void* x, int64_t ldx, const int* colmap, int kk, int rows, int dtype, void* xb,
                 cudaStream_t st);
 int grid_params(const float* w, int oc, int m, int g, int bits, int steps, double amin, float* s, float* z,

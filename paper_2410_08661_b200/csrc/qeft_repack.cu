@@ -3,6 +3,8 @@
 // low nibble, 3-bit one bitstream per row padded to a byte) and the B200 tile
 // layout documented in qeft_common.cuh; plus the group-parameter / weak-column
 // packers, the input-column gather and a dequantize-to-dense debug kernel.
+#include <algorithm>
+
 #include "qeft_common.cuh"
 #include "qeft_internal.h"
 
@@ -138,6 +140,85 @@ __global__ void gather_cols_kernel(const T* __restrict__ x, int64_t ldx, const i
   xb[idx] = c >= 0 ? x[(int64_t)t * ldx + c] : from_f32<T>(0.f);
 }
 
+// Row-staged column gather for the GEMM's B200 K order: a CTA loads one source row (src_cols
+// elements, 16-byte vectors) into shared memory, then writes the gathered row 8 elements per
+// thread (colmap read as two int4, one 16-byte store). kk % 8 == 0.
+template <typename T>
+__global__ void __launch_bounds__(256) gather_rows_kernel(const T* __restrict__ x, int64_t ldx, int src_cols,
+                                                          const int* __restrict__ colmap, int kk, int rows,
+                                                          T* __restrict__ xb, int vec) {
+  extern __shared__ __align__(16) uint8_t sm_raw[];
+  T* row = reinterpret_cast<T*>(sm_raw);
+  const T zero = from_f32<T>(0.f);
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    const T* src = x + (int64_t)r * ldx;
+    __syncthreads();  // previous row consumed
+    if (vec) {
+      for (int i = threadIdx.x; i < src_cols / 8; i += blockDim.x)
+        reinterpret_cast<uint4*>(row)[i] = reinterpret_cast<const uint4*>(src)[i];
+    } else {
+      for (int i = threadIdx.x; i < src_cols; i += blockDim.x) row[i] = src[i];
+    }
+    __syncthreads();
+    T* dst = xb + (int64_t)r * kk;
+    for (int j8 = threadIdx.x; j8 < kk / 8; j8 += blockDim.x) {
+      const int4 c0 = reinterpret_cast<const int4*>(colmap)[2 * j8];
+      const int4 c1 = reinterpret_cast<const int4*>(colmap)[2 * j8 + 1];
+      const int cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+      uint4 o;
+      T* oe = reinterpret_cast<T*>(&o);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) oe[e] = cs[e] >= 0 ? row[cs[e]] : zero;
+      reinterpret_cast<uint4*>(dst)[j8] = o;
+    }
+  }
+}
+
+// Inverse: out[r][c] (+)= xb[r][j] for colmap[j] = c (the dX of a non-structured layer, written
+// by the GEMM in B200 order). The CTA builds the inverse map in shared memory once, then per
+// row stages the B200-order row and writes the output row 8 columns per thread.
+template <typename T>
+__global__ void __launch_bounds__(256) scatter_rows_kernel(const T* __restrict__ xb, int kk,
+                                                           const int* __restrict__ colmap, int ic, int rows,
+                                                           T* __restrict__ out, int64_t ldo, int accumulate,
+                                                           int vec) {
+  extern __shared__ __align__(16) uint8_t sm_raw[];
+  int* inv = reinterpret_cast<int*>(sm_raw);
+  T* row = reinterpret_cast<T*>(sm_raw + (size_t)((ic + 3) / 4) * 16);
+  for (int c = threadIdx.x; c < ic; c += blockDim.x) inv[c] = -1;
+  __syncthreads();
+  for (int j = threadIdx.x; j < kk; j += blockDim.x) {
+    const int c = colmap[j];
+    if (c >= 0 && c < ic) inv[c] = j;
+  }
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    __syncthreads();
+    const uint4* src = reinterpret_cast<const uint4*>(xb + (int64_t)r * kk);
+    for (int i = threadIdx.x; i < kk / 8; i += blockDim.x) reinterpret_cast<uint4*>(row)[i] = src[i];
+    __syncthreads();
+    T* dst = out + (int64_t)r * ldo;
+    if (vec) {
+      for (int c8 = threadIdx.x; c8 < ic / 8; c8 += blockDim.x) {
+        uint4 o = accumulate ? reinterpret_cast<const uint4*>(dst)[c8] : make_uint4(0u, 0u, 0u, 0u);
+        T* oe = reinterpret_cast<T*>(&o);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int j = inv[8 * c8 + e];
+          const float v = j >= 0 ? to_f32<T>(row[j]) : 0.f;
+          oe[e] = from_f32<T>(accumulate ? to_f32<T>(oe[e]) + v : v);
+        }
+        reinterpret_cast<uint4*>(dst)[c8] = o;
+      }
+    } else {
+      for (int c = threadIdx.x; c < ic; c += blockDim.x) {
+        const int j = inv[c];
+        const float v = j >= 0 ? to_f32<T>(row[j]) : 0.f;
+        dst[c] = from_f32<T>(accumulate ? to_f32<T>(dst[c]) + v : v);
+      }
+    }
+  }
+}
+
 inline unsigned nblk(int64_t n, int b = 256) { return (unsigned)((n + b - 1) / b); }
 
 }  // namespace
@@ -206,6 +287,53 @@ int dequant_full(const qeft_linear_t* L, float* out, cudaStream_t st) {
     dequant_full_kernel<__half><<<nblk(n), 256, 0, st>>>(*L, out);
   else
     dequant_full_kernel<__nv_bfloat16><<<nblk(n), 256, 0, st>>>(*L, out);
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int gather_rows(const void* x, int64_t ldx, int src_cols, const int* colmap, int kk, int rows, int dtype,
+                void* xb, cudaStream_t st) {
+  if ((int64_t)rows * kk == 0) return 0;
+  const size_t smem = (size_t)src_cols * 2 + 16;
+  if (kk % 8 != 0 || (((uintptr_t)colmap) & 15) != 0 || (((uintptr_t)xb) & 15) != 0 || smem > 200 * 1024)
+    return gather_cols(x, ldx, colmap, kk, rows, dtype, xb, st);
+  const int vec = ldx % 8 == 0 && src_cols % 8 == 0 && (((uintptr_t)x) & 15) == 0;
+  const int grid = std::min(rows, 148 * 4);
+  auto go = [&](auto tag) {
+    using T = decltype(tag);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gather_rows_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    gather_rows_kernel<T><<<grid, 256, smem, st>>>((const T*)x, ldx, src_cols, colmap, kk, rows, (T*)xb, vec);
+  };
+  if (dtype == QEFT_F16) go(__half{});
+  else go(__nv_bfloat16{});
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int scatter_rows(const void* xb, int kk, const int* colmap, int ic, int rows, int dtype, void* out, int64_t ldo,
+                 int accumulate, cudaStream_t st) {
+  if ((int64_t)rows * ic == 0) return 0;
+  const size_t smem = (size_t)((ic + 3) / 4) * 16 + (size_t)kk * 2;
+  QEFT_CHECK(kk % 8 == 0 && (((uintptr_t)xb) & 15) == 0 && smem <= 200 * 1024, QEFT_ERR_SHAPE,
+             "scatter_rows: kk=%d ic=%d", kk, ic);
+  const int vec = ic % 8 == 0 && ldo % 8 == 0 && (((uintptr_t)out) & 15) == 0;
+  const int grid = std::min(rows, 148 * 4);
+  auto go = [&](auto tag) {
+    using T = decltype(tag);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(scatter_rows_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    scatter_rows_kernel<T><<<grid, 256, smem, st>>>((const T*)xb, kk, colmap, ic, rows, (T*)out, ldo, accumulate,
+                                                    vec);
+  };
+  if (dtype == QEFT_F16) go(__half{});
+  else go(__nv_bfloat16{});
   QEFT_CUDA(cudaGetLastError());
   return 0;
 }
