@@ -69,6 +69,7 @@ int gemv2_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t l
   a.ldy = ldy;
   a.yflags = y_f32;
   a.m = L->m;
+  a.ic = L->ic;
   a.m_pad = L->m_pad;
   a.k = L->k;
   a.k_pad = L->k_pad;

@@ -78,6 +78,8 @@ struct G2Args {
   int J;        // row-blocks per cluster
   int xs_ld;    // staged x row stride (elements)
   int64_t rbb;  // qweight bytes per row-block
+  int ic;        // input columns (the raw x row staged for column-map gathers)
+  int xraw_off;  // byte offset of the raw x rows in shared memory (0: gather from global memory)
   int contig;   // stages dealt to warps as contiguous runs (partials: J + NW slots) instead of
                 // round-robin (J x NW slots)
   unsigned long long* trace;  // profiling only (qeft_gemv_trace): per-CTA timestamps, or null
@@ -265,6 +267,40 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
       }
       mbar_wait(&xbar, 0);
       if (tr && threadIdx.x == 0) tr[5] = gtime();
+    } else if (a.xraw_off) {
+      // column map (irregular / online layouts): the raw x rows land in shared memory by bulk
+      // copy (ahead of the weight stream), the column map is read meanwhile, then the gather
+      // runs shared -> shared
+      T* xraw = reinterpret_cast<T*>(smem + a.xraw_off);
+      const int icp = (a.ic + 7) & ~7;
+      if (threadIdx.x == 0) {
+        mbar_expect_tx(&xbar, (uint32_t)n * a.ic * 2u);
+        for (int r = 0; r < n; ++r) bulk_g2s(xraw + r * icp, x + r * a.ldx, (uint32_t)a.ic * 2u, &xbar);
+      }
+      __syncthreads();  // x goes into the copy queue ahead of the weight stream
+      if (lane == 0)
+        while (issued < R && issue(false)) {
+        }
+      constexpr int kPer = 12;  // columns per thread held in registers while x lands
+      const int nthr = NW * 32;
+      int cols[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int c = threadIdx.x + u * nthr;
+        cols[u] = c < ncols ? a.colmap[kb + c] : -1;
+      }
+      mbar_wait(&xbar, 0);
+      for (int r = 0; r < n; ++r) {
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const int c = threadIdx.x + u * nthr;
+          if (c < ncols) xs[r * a.xs_ld + c] = cols[u] >= 0 ? xraw[r * icp + cols[u]] : zero;
+        }
+        for (int c = threadIdx.x + kPer * nthr; c < ncols; c += nthr) {
+          const int col = a.colmap[kb + c];
+          xs[r * a.xs_ld + c] = col >= 0 ? xraw[r * icp + col] : zero;
+        }
+      }
     } else {
       if (lane == 0)
         while (issued < R && issue(false)) {
@@ -691,6 +727,13 @@ int launch2(G2Args a, cudaStream_t st) {
       if (b.J > kMaxJ) break;
       const int slots = a.contig ? b.J + NW : b.J * NW;
       smem = (size_t)rings + (size_t)slots * 16 * a.n * 4 + (size_t)a.n * b.xs_ld * 2 + (size_t)xg * NT * 8 * 4;
+      b.xraw_off = 0;
+      if (!a.fast && a.ic % 8 == 0 && a.ldx % 8 == 0 && (((uintptr_t)a.x) & 15) == 0 &&
+          smem + 16 + (size_t)a.n * ((a.ic + 7) & ~7) * 2 <= (size_t)kSmemMax) {
+        smem = (smem + 15) & ~(size_t)15;
+        b.xraw_off = (int)smem;
+        smem += (size_t)a.n * ((a.ic + 7) & ~7) * 2;
+      }
       if (smem > (size_t)kSmemMax) break;
       if (S == 1) break;
       cudaLaunchConfig_t cfg = {};
