@@ -118,7 +118,7 @@ class QEFTDecoder(torch.nn.Module):
             return torch.as_tensor(np.asarray(a, np.float32)).to(device)
         blocks = []
         for i, b in enumerate(qm.blocks):
-            layers = {nm: QEFTLinear.from_quantized(b.layers[nm], dtype=act_dtype, name=f"b{i}.{nm}")
+            layers = {nm: QEFTLinear.from_quantized(b.layers[nm], dtype=act_dtype, name=f"b{i}.{nm}", device=device)
                       for nm in BLOCK_LINEARS}
             blocks.append(QEFTBlock(t(b.gain1), t(b.gain2), layers))
         return cls(qm.config, t(qm.embedding), blocks, t(qm.final_gain), t(qm.head), compute_dtype)

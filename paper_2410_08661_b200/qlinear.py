@@ -93,8 +93,8 @@ class QEFTLinear(torch.nn.Module):
         self.grad_ready_hook = None  # called after this layer's dW_weak lands in .grad
 
     @classmethod
-    def from_quantized(cls, q, dtype="bf16", name="", trainable=True):
-        return cls(DeviceLayer.from_quantized(q, dtype=dtype), name=name, trainable=trainable)
+    def from_quantized(cls, q, dtype="bf16", name="", trainable=True, device="cuda"):
+        return cls(DeviceLayer.from_quantized(q, dtype=dtype, device=device), name=name, trainable=trainable)
 
     def forward(self, x):
         if x.shape[-1] != self.ic:
