@@ -137,6 +137,15 @@ int qeft_gemv_multi(const qeft_linear_t* const* layers, int n_layers, const void
                     void* const* ys, int64_t ldy, int y_f32, int n_cols, void* workspace,
                     size_t workspace_bytes, void* stream);
 
+/* The same launch with x first RMS-normalised (model.py:249-256: x * rsqrt(mean(x^2) + 1e-5)
+ * * gain, fp32 gain [ic], the result rounded to the activation dtype) -- bit-identical to
+ * qeft_rmsnorm_fwd followed by qeft_gemv_multi; the norm runs inside the GEMV's x staging
+ * (or, when that plan cannot host it, as the stand-alone kernel into the workspace, which then
+ * needs ldx == ic). Used by the decode step for q/k/v and gate/up. */
+int qeft_gemv_multi_rmsnorm(const qeft_linear_t* const* layers, int n_layers, const void* x, int64_t ldx,
+                            const float* gain, void* const* ys, int64_t ldy, int y_f32, int n_cols,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- prefill / fine-tune GEMMs on tcgen05 (tuning.py:52-103) ----
  * fwd:   y[t][o]  = sum_i W_hat[o][i] x[t][i]                       (qlinear_forward_train)
  * dgrad: dx[t][i] = sum_o W_hat[o][i] dy[t][o]  (+= if accumulate)  (qlinear_backward dX)

@@ -111,6 +111,14 @@ int qeft_gemv(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64
   return gemv(L, x, ldx, y, ldy, y_f32, n, ws, wsb, ST(s));
 }
 
+int qeft_gemv_multi_rmsnorm(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ldx, const float* gain,
+                            void* const* ys, int64_t ldy, int y_f32, int n, void* ws, size_t wsb, void* s) {
+  QEFT_CHECK(Ls != nullptr && ys != nullptr && nl >= 1 && gain != nullptr, QEFT_ERR_SHAPE, "gemv_multi_rmsnorm: args");
+  for (int l = 0; l < nl; ++l)
+    if (int r = check_layer(Ls[l])) return r;
+  return gemv_multi(Ls, nl, x, ldx, ys, ldy, y_f32, n, ws, wsb, ST(s), gain);
+}
+
 int qeft_gemv_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ldx, void* const* ys,
                     int64_t ldy, int y_f32, int n, void* ws, size_t wsb, void* s) {
   QEFT_CHECK(Ls != nullptr && ys != nullptr && nl >= 1, QEFT_ERR_SHAPE, "gemv_multi: no layers");

@@ -661,13 +661,18 @@ namespace qeft {
 //             [split-K partials (bulk-copy path) | x gather buffer (generic path)].
 constexpr size_t kWsHead = 64 * 1024;
 
+// (+ the fused RMS-norm's fallback: normalized x [n][ic] and rstd [n] behind the gather buffer)
+static size_t norm_ws_bytes(const qeft_linear_t* L, int n) { return (size_t)n * L->ic * 2 + (size_t)n * 4 + 512; }
+static size_t gather_ws_bytes(const qeft_linear_t* L, int n) {
+  return ((size_t)n * (L->m_pad + L->k_pad) * 2 + 256 + 255) & ~(size_t)255;
+}
+
 size_t gemv_workspace_bytes(const qeft_linear_t* L, int n) {
-  const size_t gather = (size_t)n * (L->m_pad + L->k_pad) * 2 + 256;
-  return std::max(gemv2_workspace_bytes(L, n), kWsHead + gather);
+  return std::max(gemv2_workspace_bytes(L, n), kWsHead + gather_ws_bytes(L, n) + norm_ws_bytes(L, n));
 }
 
 int gemv_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ldx, void* const* ys, int64_t ldy,
-               int y_f32, int n, void* ws, size_t ws_bytes, cudaStream_t st) {
+               int y_f32, int n, void* ws, size_t ws_bytes, cudaStream_t st, const float* ngain) {
   QEFT_CHECK(nl >= 1 && nl <= kMaxLayers, QEFT_ERR_SHAPE, "gemv: %d layers per launch (1..%d)", nl, kMaxLayers);
   const qeft_linear_t* L = Ls[0];
   QEFT_CHECK(n >= 1 && n <= 16, QEFT_ERR_SHAPE, "gemv: n_cols=%d outside 1..16", n);
@@ -696,8 +701,18 @@ int gemv_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ld
   // bulk-copy warp-ring kernel (qeft_gemv2.cu) for group sizes that are multiples of 64;
   // the per-element-dequant kernel below otherwise
   if (v2) {
-    const int r = gemv2_multi(Ls, nl, x, ldx, ys, ldy, y_f32, n, ws, ws_bytes, st);
+    const int r = gemv2_multi(Ls, nl, x, ldx, ys, ldy, y_f32, n, ws, ws_bytes, st, ngain);
     if (r != -1) return r;
+  }
+  if (ngain) {
+    // the fused norm did not fit this launch: the stand-alone kernel, then the plain GEMV
+    const size_t off = kWsHead + gather_ws_bytes(L, n);
+    QEFT_CHECK(ws_bytes >= off + norm_ws_bytes(L, n) && ldx == L->ic, QEFT_ERR_SHAPE,
+               "gemv: workspace too small for the RMS-norm (or ldx != ic)");
+    uint8_t* xn = (uint8_t*)ws + off;
+    float* rstd = (float*)(xn + (((size_t)n * L->ic * 2 + 255) & ~(size_t)255));
+    if (int r = rmsnorm_fwd(x, ngain, xn, rstd, n, L->ic, L->act_dtype, st)) return r;
+    return gemv_multi(Ls, nl, xn, L->ic, ys, ldy, y_f32, n, ws, ws_bytes, st, nullptr);
   }
   QEFT_CHECK(ws_bytes >= kWsHead, QEFT_ERR_SHAPE, "gemv: workspace too small");
   ws = (uint8_t*)ws + kWsHead;  // never touch the bulk-copy path's counters

@@ -79,6 +79,8 @@ struct G2Args {
   int xs_ld;    // staged x row stride (elements)
   int64_t rbb;  // qweight bytes per row-block
   int ic;        // input columns (the raw x row staged for column-map gathers)
+  const float* ngain;  // fused RMS-norm of x (model.py:249-256): gain [ic] fp32, or null
+  int nthr;            // the stand-alone rmsnorm kernel's block size (its reduction order is kept)
   int xraw_off;  // byte offset of the raw x rows in shared memory (0: gather from global memory)
   int contig;   // stages dealt to warps as contiguous runs (partials: J + NW slots) instead of
                 // round-robin (J x NW slots)
@@ -332,6 +334,54 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
     }
   }
   __syncthreads();
+  if (a.ngain) {
+    // fused RMS-norm of the staged x, bit-identical to qeft_rmsnorm_fwd: the first nthr threads
+    // sum x^2 in that kernel's order (8 consecutive columns per thread, stride nthr * 8, warp
+    // shuffles, then across warps), read from the staged row when it holds every column
+    // (structured, one K slice), else from the raw row / global x; then y = gain * x * rstd.
+    __shared__ float s_nred[32];
+    __shared__ float s_rstd[16];
+    const T* xg = reinterpret_cast<const T*>(a.x);
+    const T* xraw = reinterpret_cast<const T*>(smem + a.xraw_off);
+    const int icp = (a.ic + 7) & ~7;
+    const bool from_xs = a.fast && a.S == 1;
+    for (int r = 0; r < n; ++r) {
+      float ss = 0.f;
+      if ((int)threadIdx.x < a.nthr) {
+        for (int c = threadIdx.x * 8; c < a.ic; c += a.nthr * 8) {
+          uint4 v;
+          if (from_xs) v = lds128(xs + r * a.xs_ld + (c < a.m ? c : a.m_pad + (c - a.m)) - kb);
+          else if (a.xraw_off) v = lds128(xraw + r * icp + c);
+          else v = *reinterpret_cast<const uint4*>(xg + r * a.ldx + c);
+          const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float f = to_f32<T>(e[i]);
+            ss += f * f;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) s_nred[warp] = ss;
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        float v = (int)threadIdx.x < (a.nthr >> 5) ? s_nred[threadIdx.x] : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) s_rstd[r] = rsqrtf(v / (float)a.ic + 1e-5f);
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < n * ncols; e += NW * 32) {
+      const int r = ONE ? 0 : e / ncols, c = e - r * ncols, p = kb + c;
+      int col;
+      if (a.fast) col = p < a.m ? p : ((p >= a.m_pad && p < a.m_pad + a.k) ? a.m + (p - a.m_pad) : -1);
+      else col = a.colmap[p];
+      if (col >= 0) xs[r * a.xs_ld + c] = from_f32<T>(a.ngain[col] * to_f32<T>(xs[r * a.xs_ld + c]) * s_rstd[r]);
+    }
+    __syncthreads();
+  }
   // per-(group, column) sums of x over the staged quantized columns: 16 lanes per pair,
   // fixed-order tree reduction (deterministic)
   const int gx0 = sg.gx0, ngx = sg.ngx;
@@ -660,6 +710,7 @@ template <int BITS, int NT, int GT, typename T, int R, int NW, int CPS, bool CON
           int GPS = MINB>
 int launch2(G2Args a, cudaStream_t st) {
   a.contig = CONTIG;
+  if (a.ngain && NW * 32 < a.nthr) return -1;  // the fused norm needs the rmsnorm block size
   constexpr int kStage = CPS * 1152;
   constexpr int kSmemMax = (MINB == 1 ? 227 * 1024 : 113 * 1024) - 1024;
   constexpr int PRE = MINB > 1 ? R : 0;  // pre-wait weight prefetch only when CTAs can overlap

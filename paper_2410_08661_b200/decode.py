@@ -63,9 +63,11 @@ def random_layer(oc, ic, k=128, bits=4, g=128, dtype="f16", seed=0, device="cuda
                        sz16=make_sz16(s[:oc].float(), z[:oc].float(), oc, m, g))
 
 
-def gemv_multi(layers, x, outs):
+def gemv_multi(layers, x, outs, norm_gain=None):
     """One decode-GEMV launch over layers that read the same x (qeft_gemv_multi): a
-    decoder's q/k/v or gate/up. outs[l] is layer l's (n, oc_l) output."""
+    decoder's q/k/v or gate/up. outs[l] is layer l's (n, oc_l) output. norm_gain (fp32 [ic]):
+    x is RMS-normalised inside the launch first (qeft_gemv_multi_rmsnorm), bit-identical to
+    fused.rms_norm followed by this call."""
     n = x.shape[0]
     L = _lib.lib()
     arr = (ctypes.POINTER(_lib.QeftLinearT) * len(layers))(*[l.cptr for l in layers])
@@ -76,9 +78,15 @@ def gemv_multi(layers, x, outs):
     wsb = sum(int(L.qeft_gemv_workspace_bytes(l.cptr, n)) for l in layers)
     ws = GEMV_WORKSPACE.get(wsb, x.device)
     ldx = x.stride(0) if n > 1 else layers[0].ic
+    yf = 1 if outs[0].dtype.itemsize == 4 else 0
+    if norm_gain is not None:
+        g = norm_gain.contiguous().float()
+        _lib.check(L.qeft_gemv_multi_rmsnorm(ctypes.cast(arr, ctypes.c_void_p), len(layers), _lib.ptr(x), ldx,
+                                             _lib.ptr(g), ctypes.cast(ys, ctypes.c_void_p), ldy, yf, n,
+                                             _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "gemv_multi_rmsnorm")
+        return outs
     _lib.check(L.qeft_gemv_multi(ctypes.cast(arr, ctypes.c_void_p), len(layers), _lib.ptr(x), ldx,
-                                 ctypes.cast(ys, ctypes.c_void_p), ldy,
-                                 1 if outs[0].dtype.itemsize == 4 else 0, n, _lib.ptr(ws), ws.numel(),
+                                 ctypes.cast(ys, ctypes.c_void_p), ldy, yf, n, _lib.ptr(ws), ws.numel(),
                                  _lib.stream_ptr()), "gemv_multi")
     return outs
 

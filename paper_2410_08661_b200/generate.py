@@ -82,14 +82,18 @@ class KVDecoder:
         dyn = isinstance(pos, torch.Tensor)
         x = F.embedding(tok, self.emb).contiguous()  # (B, d) residual stream, updated in place
         if dyn:
-            keep = (torch.arange(self.T, device=tok.device) <= pos).view(1, 1, 1, self.T)
+            # additive mask (0 / -inf) built once per step: a boolean mask would be converted
+            # (fill + masked_fill) inside every block's attention call
+            keep = torch.zeros(1, 1, 1, self.T, dtype=self.dt, device=tok.device).masked_fill_(
+                (torch.arange(self.T, device=tok.device) > pos).view(1, 1, 1, self.T), float("-inf"))
         for i, blk in enumerate(self.model.blocks):
-            a = fused.rms_norm(x, blk.gain1)
             if self.qkv_fused[i]:
+                # the RMS-norm runs inside the q/k/v launch's x staging
                 q = torch.empty(B, blk.wq.oc, dtype=self.dt, device=x.device)
                 k, v = torch.empty_like(q), torch.empty(B, blk.wv.oc, dtype=self.dt, device=x.device)
-                decode.gemv_multi([blk.wq.dl, blk.wk.dl, blk.wv.dl], a, [q, k, v])
+                decode.gemv_multi([blk.wq.dl, blk.wk.dl, blk.wv.dl], x, [q, k, v], norm_gain=blk.gain1)
             else:
+                a = fused.rms_norm(x, blk.gain1)
                 q, k, v = blk.wq.dl.gemv(a), blk.wk.dl.gemv(a), blk.wv.dl.gemv(a)
             kc, vc = self.k_cache[i], self.v_cache[i]
             # rotary on q and k + the cache append at the device position, one kernel
@@ -102,12 +106,12 @@ class KVDecoder:
                                                    scale=1.0 / math.sqrt(hd))
             x = x.contiguous()
             blk.wo.dl.gemv(o.transpose(1, 2).reshape(B, H * hd), out=x, accumulate=True)  # x += Wo o
-            b2 = fused.rms_norm(x, blk.gain2)
             if self.gu_fused[i]:
                 gt = torch.empty(B, blk.w_gate.oc, dtype=self.dt, device=x.device)
                 up = torch.empty_like(gt)
-                decode.gemv_multi([blk.w_gate.dl, blk.w_up.dl], b2, [gt, up])
+                decode.gemv_multi([blk.w_gate.dl, blk.w_up.dl], x, [gt, up], norm_gain=blk.gain2)
             else:
+                b2 = fused.rms_norm(x, blk.gain2)
                 gt, up = blk.w_gate.dl.gemv(b2), blk.w_up.dl.gemv(b2)
             blk.w_down.dl.gemv(fused.silu_mul(gt, up), out=x, accumulate=True)  # x += Wdown f
         z = fused.rms_norm(x, self.model.final_gain)

@@ -293,3 +293,32 @@ def test_gemv_accumulate_epilogue(B):
         yf = y0.float().clone()
         dl.gemv(x, out=yf, accumulate=True)
         assert rel_err(yf.cpu().numpy(), ref.cpu().numpy()) <= 1e-6
+
+
+@pytest.mark.parametrize("oc,ic,layout,n", [(1024, 4096, "structured", 1), (1024, 4096, "structured", 8),
+                                            (512, 4096, "structured", 16), (512, 4096, "irregular", 1),
+                                            (256, 8192, "structured", 1)])
+def test_gemv_multi_fused_rmsnorm_bit_identical(B, oc, ic, layout, n):
+    """qeft_gemv_multi_rmsnorm (the norm inside the GEMV's x staging: one K slice, cluster K
+    slices at n = 16, the column-map layout, and the stand-alone fallback at IC 8192) equals
+    fused.rms_norm followed by qeft_gemv_multi bit for bit (model.py:249-256)."""
+    import torch
+    from paper_2410_08661_b200 import decode, fused
+    quantizer = B[4]
+    if layout == "structured":
+        dls = [decode.random_layer(oc, ic, 128, 4, 128, "f16", seed=s) for s in range(2)]
+    else:  # column-map layers share x only through one colmap: one layer per launch
+        rng = np.random.default_rng(oc + ic)
+        w = (rng.standard_normal((oc, ic)) * 0.02).astype(np.float32)
+        q = quantizer.quantize_layer(w, k=64, bits=4, g=128, mode="rtn", layout="irregular",
+                                     lam=np.abs(rng.standard_normal(ic)))
+        dls = [q.device("f16")]
+    x = (torch.randn(n, ic, device="cuda") * 3).half()
+    gain = torch.rand(ic, device="cuda") + 0.5
+    ya = [torch.empty(n, oc, dtype=torch.float16, device="cuda") for _ in dls]
+    yb = [torch.empty_like(y) for y in ya]
+    decode.gemv_multi(dls, x, ya, norm_gain=gain)
+    decode.gemv_multi(dls, fused.rms_norm(x, gain), yb)
+    torch.cuda.synchronize()
+    for a_, b_ in zip(ya, yb):
+        assert torch.equal(a_, b_), (a_.float() - b_.float()).abs().max()
