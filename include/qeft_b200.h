@@ -146,6 +146,13 @@ int qeft_gemv_multi_rmsnorm(const qeft_linear_t* const* layers, int n_layers, co
                             const float* gain, void* const* ys, int64_t ldy, int y_f32, int n_cols,
                             void* workspace, size_t workspace_bytes, void* stream);
 
+/* y (+)= W_hat (silu(g) * u) for g, u of shape (n, ic), common row pitch ldx (the decode step's
+ * down projection over the gate / up outputs, model.py:389-391) -- bit-identical to
+ * qeft_silu_mul_fwd followed by qeft_gemv; structured layers combine g and u inside the x
+ * staging, other layouts run the stand-alone kernel into the workspace (ldx == ic). */
+int qeft_gemv_swiglu(const qeft_linear_t* layer, const void* g, const void* u, int64_t ldx, void* y, int64_t ldy,
+                     int y_flags, int n_cols, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- prefill / fine-tune GEMMs on tcgen05 (tuning.py:52-103) ----
  * fwd:   y[t][o]  = sum_i W_hat[o][i] x[t][i]                       (qlinear_forward_train)
  * dgrad: dx[t][i] = sum_o W_hat[o][i] dy[t][o]  (+= if accumulate)  (qlinear_backward dX)

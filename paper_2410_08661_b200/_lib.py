@@ -55,6 +55,7 @@ SIGNATURES = {
     "qeft_gemv_trace": (_I, [_I, _VP]),
     "qeft_gemm_set_schedule": (_I, [_I, _I]),
     "qeft_gemv_multi_rmsnorm": (_I, [_VP, _I, _VP, _I64, _VP, _VP, _I64, _I, _I, _VP, _SZ, _VP]),
+    "qeft_gemv_swiglu": (_I, [_LP, _VP, _VP, _I64, _VP, _I64, _I, _I, _VP, _SZ, _VP]),
     "qeft_gemv_workspace_bytes": (_SZ, [_LP, _I]),
     "qeft_gemv": (_I, [_LP, _VP, _I64, _VP, _I64, _I, _I, _VP, _SZ, _VP]),
     "qeft_gemv_multi": (_I, [_VP, _I, _VP, _I64, _VP, _I64, _I, _I, _VP, _SZ, _VP]),

@@ -111,6 +111,13 @@ int qeft_gemv(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64
   return gemv(L, x, ldx, y, ldy, y_f32, n, ws, wsb, ST(s));
 }
 
+int qeft_gemv_swiglu(const qeft_linear_t* L, const void* g, const void* u, int64_t ldx, void* y, int64_t ldy,
+                     int y_flags, int n, void* ws, size_t wsb, void* s) {
+  if (int r = check_layer(L)) return r;
+  QEFT_CHECK(g != nullptr && u != nullptr, QEFT_ERR_SHAPE, "gemv_swiglu: null input");
+  return gemv_multi(&L, 1, g, ldx, &y, ldy, y_flags, n, ws, wsb, ST(s), nullptr, u);
+}
+
 int qeft_gemv_multi_rmsnorm(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ldx, const float* gain,
                             void* const* ys, int64_t ldy, int y_f32, int n, void* ws, size_t wsb, void* s) {
   QEFT_CHECK(Ls != nullptr && ys != nullptr && nl >= 1 && gain != nullptr, QEFT_ERR_SHAPE, "gemv_multi_rmsnorm: args");

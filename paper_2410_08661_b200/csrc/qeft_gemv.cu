@@ -672,7 +672,7 @@ size_t gemv_workspace_bytes(const qeft_linear_t* L, int n) {
 }
 
 int gemv_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ldx, void* const* ys, int64_t ldy,
-               int y_f32, int n, void* ws, size_t ws_bytes, cudaStream_t st, const float* ngain) {
+               int y_f32, int n, void* ws, size_t ws_bytes, cudaStream_t st, const float* ngain, const void* xu) {
   QEFT_CHECK(nl >= 1 && nl <= kMaxLayers, QEFT_ERR_SHAPE, "gemv: %d layers per launch (1..%d)", nl, kMaxLayers);
   const qeft_linear_t* L = Ls[0];
   QEFT_CHECK(n >= 1 && n <= 16, QEFT_ERR_SHAPE, "gemv: n_cols=%d outside 1..16", n);
@@ -701,8 +701,17 @@ int gemv_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ld
   // bulk-copy warp-ring kernel (qeft_gemv2.cu) for group sizes that are multiples of 64;
   // the per-element-dequant kernel below otherwise
   if (v2) {
-    const int r = gemv2_multi(Ls, nl, x, ldx, ys, ldy, y_f32, n, ws, ws_bytes, st, ngain);
+    const int r = gemv2_multi(Ls, nl, x, ldx, ys, ldy, y_f32, n, ws, ws_bytes, st, ngain, xu);
     if (r != -1) return r;
+  }
+  if (xu) {
+    // the fused SwiGLU did not fit this launch: the stand-alone kernel, then the plain GEMV
+    const size_t off = kWsHead + gather_ws_bytes(L, n);
+    QEFT_CHECK(ws_bytes >= off + norm_ws_bytes(L, n) && ldx == L->ic, QEFT_ERR_SHAPE,
+               "gemv: workspace too small for the SwiGLU (or ldx != ic)");
+    uint8_t* f = (uint8_t*)ws + off;
+    if (int r = silu_mul_fwd(x, xu, f, (int64_t)n * L->ic, L->act_dtype, st)) return r;
+    return gemv_multi(Ls, nl, f, L->ic, ys, ldy, y_f32, n, ws, ws_bytes, st, ngain, nullptr);
   }
   if (ngain) {
     // the fused norm did not fit this launch: the stand-alone kernel, then the plain GEMV

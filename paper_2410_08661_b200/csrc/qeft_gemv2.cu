@@ -46,7 +46,7 @@ int gemv_trace(int slots, unsigned long long* host_out) {
 }
 
 int gemv2_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ldx, void* const* ys, int64_t ldy,
-                int y_f32, int n, void*, size_t, cudaStream_t st, const float* ngain) {
+                int y_f32, int n, void*, size_t, cudaStream_t st, const float* ngain, const void* xu) {
   const qeft_linear_t* L = Ls[0];
   G2Args a{};
   a.nl = nl;
@@ -70,6 +70,11 @@ int gemv2_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t l
   a.yflags = y_f32;
   a.m = L->m;
   a.ic = L->ic;
+  if (xu) {
+    // fused SwiGLU: structured layers (x moved by bulk copies), 16-byte aligned rows
+    if (!a.fast || (((uintptr_t)xu) & 15) != 0) return -1;
+    a.xu = xu;
+  }
   if (ngain) {
     // fused RMS-norm: 16-byte rows (the stand-alone kernel's layout), its block size kept
     if (L->ic % 8 != 0 || ldx % 8 != 0 || (((uintptr_t)x) & 15) != 0) return -1;

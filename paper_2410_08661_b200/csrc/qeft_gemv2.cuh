@@ -79,6 +79,8 @@ struct G2Args {
   int xs_ld;    // staged x row stride (elements)
   int64_t rbb;  // qweight bytes per row-block
   int ic;        // input columns (the raw x row staged for column-map gathers)
+  const void* xu;      // fused SwiGLU input (model.py:389-391): x = silu(x) * xu (structured layers)
+  int xu_off;          // byte offset of the staged xu rows in shared memory
   const float* ngain;  // fused RMS-norm of x (model.py:249-256): gain [ic] fp32, or null
   int nthr;            // the stand-alone rmsnorm kernel's block size (its reduction order is kept)
   int xraw_off;  // byte offset of the raw x rows in shared memory (0: gather from global memory)
@@ -244,12 +246,20 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
         const uint32_t bytes =
             (uint32_t)n * 2u * (uint32_t)(max(q1 - kb, 0) + max(w_end - w_beg, 0));
         if (bytes) {
-          mbar_expect_tx(&xbar, bytes);
+          T* xus = reinterpret_cast<T*>(smem + a.xu_off);
+          const T* xu = reinterpret_cast<const T*>(a.xu);
+          mbar_expect_tx(&xbar, a.xu ? 2 * bytes : bytes);
           for (int r = 0; r < n; ++r) {
             if (q1 > kb) bulk_g2s(xs + r * a.xs_ld, x + r * a.ldx + kb, (uint32_t)(q1 - kb) * 2u, &xbar);
             if (w_end > w_beg)
               bulk_g2s(xs + r * a.xs_ld + (w_beg - kb), x + r * a.ldx + a.m + (w_beg - a.m_pad),
                        (uint32_t)(w_end - w_beg) * 2u, &xbar);
+            if (a.xu) {
+              if (q1 > kb) bulk_g2s(xus + r * a.xs_ld, xu + r * a.ldx + kb, (uint32_t)(q1 - kb) * 2u, &xbar);
+              if (w_end > w_beg)
+                bulk_g2s(xus + r * a.xs_ld + (w_beg - kb), xu + r * a.ldx + a.m + (w_beg - a.m_pad),
+                         (uint32_t)(w_end - w_beg) * 2u, &xbar);
+            }
           }
         } else {
           mbar_arrive(&xbar);
@@ -268,6 +278,17 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
         xs[r * a.xs_ld + (c < nz0 ? z0a + c : z1a + c - nz0) - kb] = zero;
       }
       mbar_wait(&xbar, 0);
+      if (a.xu) {
+        // SwiGLU in place, the stand-alone kernel's expression (bit-identical): x = silu(g) * u
+        const T* xus = reinterpret_cast<const T*>(smem + a.xu_off);
+        const int nq = max(q1 - kb, 0), nw = max(w_end - w_beg, 0);
+        for (int e = threadIdx.x; e < n * (nq + nw); e += NW * 32) {
+          const int r = ONE ? 0 : e / (nq + nw), c = e - r * (nq + nw);
+          const int o = r * a.xs_ld + (c < nq ? c : (w_beg - kb) + (c - nq));
+          const float gv = to_f32<T>(xs[o]);
+          xs[o] = from_f32<T>(gv / (1.f + __expf(-gv)) * to_f32<T>(xus[o]));
+        }
+      }
       if (tr && threadIdx.x == 0) tr[5] = gtime();
     } else if (a.xraw_off) {
       // column map (irregular / online layouts): the raw x rows land in shared memory by bulk
@@ -778,6 +799,11 @@ int launch2(G2Args a, cudaStream_t st) {
       if (b.J > kMaxJ) break;
       const int slots = a.contig ? b.J + NW : b.J * NW;
       smem = (size_t)rings + (size_t)slots * 16 * a.n * 4 + (size_t)a.n * b.xs_ld * 2 + (size_t)xg * NT * 8 * 4;
+      if (a.xu) {  // the staged up-projection rows (same layout as xs)
+        smem = (smem + 15) & ~(size_t)15;
+        b.xu_off = (int)smem;
+        smem += (size_t)a.n * b.xs_ld * 2;
+      }
       b.xraw_off = 0;
       if (!a.fast && a.ic % 8 == 0 && a.ldx % 8 == 0 && (((uintptr_t)a.x) & 15) == 0 &&
           smem + 16 + (size_t)a.n * ((a.ic + 7) & ~7) * 2 <= (size_t)kSmemMax) {

@@ -57,7 +57,8 @@ size_t gemv_workspace_bytes(const qeft_linear_t* L, int n);
 int gemv(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ldy, int y_f32, int n,
          void* ws, size_t ws_bytes, cudaStream_t st);
 int gemv_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ldx, void* const* ys, int64_t ldy,
-               int y_f32, int n, void* ws, size_t ws_bytes, cudaStream_t st, const float* ngain = nullptr);
+               int y_f32, int n, void* ws, size_t ws_bytes, cudaStream_t st, const float* ngain = nullptr,
+               const void* xu = nullptr);
 // bulk-copy warp-ring GEMV (qeft_gemv2.cu); gemv2_multi returns -1 when the launch needs the
 // generic path (its partials would not fit shared memory)
 int gemv_trace(int slots, unsigned long long* host_out);
@@ -67,7 +68,8 @@ bool gemv2_supported(const qeft_linear_t* L, int n);
 size_t gemv2_workspace_bytes(const qeft_linear_t* L, int n);
 int gemv2_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t ldx, void* const* ys,
                 int64_t ldy, int y_f32, int n, void* ws, size_t ws_bytes, cudaStream_t st,
-                const float* ngain = nullptr);
+                const float* ngain = nullptr, const void* xu = nullptr);
+int silu_mul_fwd(const void* g, const void* u, void* f, int64_t n, int dt, cudaStream_t st);
 int rmsnorm_fwd(const void* x, const float* gain, void* y, float* rstd, int rows, int C, int dt, cudaStream_t st);
 
 size_t gemm_workspace_bytes(const qeft_linear_t* L, int T);

@@ -3,13 +3,14 @@
 The reference's harness `bench_generate` (pkg/src/qeft/kernels.py:197-228) has no KV cache:
 each new token recomputes the whole prefix, every linear layer going column by column through
 its matvec path. `KVDecoder` is the B200 form of the same greedy loop. Per token and block it runs:
-  RMS-norm (qeft_rmsnorm_fwd)
-  -> q/k/v: one qeft_gemv_multi launch when the three share geometry, else per-layer qeft_gemv
+  q/k/v: one qeft_gemv_multi_rmsnorm launch when the three share geometry (the RMS-norm runs
+     in its x staging), else RMS-norm + per-layer qeft_gemv
   -> rotary on q/k at the token's position + k/v appended to the cache (one qeft_rope_kv)
   -> attention over the cache (torch SDPA, fp32 softmax inside the kernel)
   -> o (qeft_gemv, irregular / online-reorder layouts gather x in-kernel), the residual add
      fused into its epilogue (QEFT_Y_ACCUMULATE)
-  -> RMS-norm -> gate/up (one launch) -> SiLU*up (qeft_silu_mul_fwd) -> down, residual fused
+  -> gate/up (one launch, RMS-norm in its x staging) -> down over silu(gate)*up (SwiGLU in its
+     x staging, qeft_gemv_swiglu), residual fused
 The final norm and the frozen dense head follow, then argmax. Semantics follow the reference
 engine's forward (model.py:323-407): one decode step at position p equals column p of a full
 causal forward. The same greedy token choice (np.argmax: first maximum) is kept.
@@ -113,7 +114,7 @@ class KVDecoder:
             else:
                 b2 = fused.rms_norm(x, blk.gain2)
                 gt, up = blk.w_gate.dl.gemv(b2), blk.w_up.dl.gemv(b2)
-            blk.w_down.dl.gemv(fused.silu_mul(gt, up), out=x, accumulate=True)  # x += Wdown f
+            blk.w_down.dl.gemv_swiglu(gt, up, out=x, accumulate=True)  # x += Wdown (silu(gt) * up)
         z = fused.rms_norm(x, self.model.final_gain)
         return (z @ self.head.t()).float()  # (B, V) fp32 logits
 

@@ -202,6 +202,30 @@ class DeviceLayer:
                                ws.numel(), _lib.stream_ptr()), "gemv")
         return out
 
+    def gemv_swiglu(self, g, u, out=None, accumulate=False):
+        """y[n] = W_hat (silu(g[n]) * u[n]) (the decode step's down projection, model.py:389-391):
+        the SwiGLU runs inside the GEMV's x staging (qeft_gemv_swiglu), bit-identical to
+        fused.silu_mul followed by gemv."""
+        import torch
+        _lib.require_cuda(g, "g")
+        if g.shape != u.shape or g.dim() != 2 or g.shape[1] != self.ic or g.dtype != self.tdtype or u.dtype != g.dtype:
+            raise ShapeError(f"gemv_swiglu: g {tuple(g.shape)} / u {tuple(u.shape)} incompatible with the layer")
+        g, u = g.contiguous(), u.contiguous()
+        n = g.shape[0]
+        if out is None:
+            if accumulate:
+                raise ShapeError("gemv_swiglu: accumulate needs an output to add to")
+            out = torch.empty((n, self.oc), dtype=self.tdtype, device=g.device)
+        L = _lib.lib()
+        ws = GEMV_WORKSPACE.get(int(L.qeft_gemv_workspace_bytes(self.cptr, n)), g.device)
+        ldy = out.stride(0) if n > 1 else self.oc
+        if out.stride(1) != 1 or (n > 1 and ldy < self.oc):
+            raise ShapeError("gemv_swiglu: out must be row-major with unit column stride")
+        flags = (1 if out.dtype == torch.float32 else 0) | (2 if accumulate else 0)
+        _lib.check(L.qeft_gemv_swiglu(self.cptr, _lib.ptr(g), _lib.ptr(u), self.ic, _lib.ptr(out), ldy, flags, n,
+                                      _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "gemv_swiglu")
+        return out
+
     def gemm_fwd(self, x, out=None):
         """y = x W_hat^T for x of shape (T, ic) (prefill / fine-tune forward)."""
         import torch

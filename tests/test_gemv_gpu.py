@@ -322,3 +322,28 @@ def test_gemv_multi_fused_rmsnorm_bit_identical(B, oc, ic, layout, n):
     torch.cuda.synchronize()
     for a_, b_ in zip(ya, yb):
         assert torch.equal(a_, b_), (a_.float() - b_.float()).abs().max()
+
+
+@pytest.mark.parametrize("oc,ic,layout,n", [(512, 11008, "structured", 1), (512, 11008, "structured", 4),
+                                            (256, 1024, "irregular", 2)])
+def test_gemv_swiglu_bit_identical(B, oc, ic, layout, n):
+    """qeft_gemv_swiglu (SwiGLU inside the down projection's x staging; the stand-alone
+    fallback for column-map layouts) equals fused.silu_mul followed by gemv bit for bit, with
+    the residual add of the epilogue (model.py:389-391)."""
+    import torch
+    from paper_2410_08661_b200 import decode, fused
+    quantizer = B[4]
+    if layout == "structured":
+        dl = decode.random_layer(oc, ic, 128, 4, 128, "f16", seed=7)
+    else:
+        rng = np.random.default_rng(oc + ic)
+        w = (rng.standard_normal((oc, ic)) * 0.02).astype(np.float32)
+        dl = quantizer.quantize_layer(w, k=64, bits=4, g=128, mode="rtn", layout="irregular",
+                                      lam=np.abs(rng.standard_normal(ic))).device("f16")
+    g = (torch.randn(n, ic, device="cuda") * 2).half()
+    u = torch.randn(n, ic, device="cuda").half()
+    y0 = torch.randn(n, oc, device="cuda").half()
+    a_ = dl.gemv_swiglu(g, u, out=y0.clone(), accumulate=True)
+    b_ = dl.gemv(fused.silu_mul(g, u), out=y0.clone(), accumulate=True)
+    torch.cuda.synchronize()
+    assert torch.equal(a_, b_), (a_.float() - b_.float()).abs().max()
