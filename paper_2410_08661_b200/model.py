@@ -24,7 +24,9 @@ import torch.nn.functional as F
 
 from . import fused
 from .errors import ShapeError
-from .qlinear import QEFTLinear
+from .qlinear import QEFTLinear, grouped_linear
+
+_GROUPED = __import__("os").environ.get("QEFT_GROUPED", "1") != "0"  # A/B knob
 from .qmodel import BLOCK_LINEARS, RMS_EPS, ROPE_BASE, ModelConfig
 
 _TD = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}
@@ -86,13 +88,20 @@ class QEFTBlock(torch.nn.Module):
         B, T, _ = x.shape
         H, hd = cfg.n_heads, cfg.head_dim
         a = fused.rms_norm(x, self.gain1)
-        q = fused.rope(self.wq(a), cos, sin, T, H, hd).view(B, T, H, hd).transpose(1, 2)
-        k = fused.rope(self.wk(a), cos, sin, T, H, hd).view(B, T, H, hd).transpose(1, 2)
-        v = self.wv(a).view(B, T, H, hd).transpose(1, 2)
+        # q/k/v (and gate/up) read the same normed input: one grouped op, whose backward sums
+        # the three dX in one buffer (GEMM reduce-add epilogue)
+        if _GROUPED:
+            qp, kp, vp = grouped_linear([self.wq, self.wk, self.wv], a)
+        else:
+            qp, kp, vp = self.wq(a), self.wk(a), self.wv(a)
+        q = fused.rope(qp, cos, sin, T, H, hd).view(B, T, H, hd).transpose(1, 2)
+        k = fused.rope(kp, cos, sin, T, H, hd).view(B, T, H, hd).transpose(1, 2)
+        v = vp.view(B, T, H, hd).transpose(1, 2)
         o = F.scaled_dot_product_attention(q, k, v, is_causal=True, scale=1.0 / math.sqrt(hd))
         x1 = x + self.wo(o.transpose(1, 2).reshape(B, T, H * hd))
         b2 = fused.rms_norm(x1, self.gain2)
-        f = fused.silu_mul(self.w_gate(b2), self.w_up(b2))
+        gt, up = grouped_linear([self.w_gate, self.w_up], b2) if _GROUPED else (self.w_gate(b2), self.w_up(b2))
+        f = fused.silu_mul(gt, up)
         return x1 + self.w_down(f)
 
 

@@ -59,6 +59,65 @@ class _QEFTLinearFn(torch.autograd.Function):
         return dx, None, None, None
 
 
+class _QEFTGroupFn(torch.autograd.Function):
+    """Several QEFT layers over the same input (a block's q/k/v, or gate/up): one forward GEMM
+    per layer; the backward sums their dX in place (qeft_gemm_dgrad accumulate, a TMA
+    reduce-add in the epilogue) instead of one autograd add per extra consumer of x."""
+
+    @staticmethod
+    def forward(ctx, x2, mods, *weaks):
+        ys, saved, idx = [], [], []
+        for i, (mod, w) in enumerate(zip(mods, weaks)):
+            dl: DeviceLayer = mod.dl
+            ys.append(dl.gemm_fwd(x2))
+            if w.requires_grad and dl.k:
+                saved.append(_weak_slice(dl, x2))
+                idx.append(i)
+        ctx.mods, ctx.widx = mods, idx
+        ctx.save_for_backward(*saved)
+        return tuple(ys)
+
+    @staticmethod
+    def backward(ctx, *dys):
+        xws = dict(zip(ctx.widx, ctx.saved_tensors))
+        dx = None
+        for i, (mod, dy) in enumerate(zip(ctx.mods, dys)):
+            if dy is None:
+                continue
+            dl: DeviceLayer = mod.dl
+            dy = dy.contiguous()
+            if dy.dtype != dl.tdtype:
+                dy = dy.to(dl.tdtype)
+            if ctx.needs_input_grad[0]:
+                dx = dl.gemm_dgrad(dy) if dx is None else dl.gemm_dgrad(dy, out=dx, accumulate=True)
+            if i in xws:
+                w = mod.weak32
+                if w.grad is None:
+                    w.grad = torch.zeros_like(w)
+                dl.gemm_wgrad_weak(dy, xws[i], out=w.grad, accumulate=True)
+                if mod.grad_ready_hook is not None:
+                    mod.grad_ready_hook(mod)
+        return (dx, None) + (None,) * len(ctx.mods)
+
+
+def grouped_linear(mods, x):
+    """(mod(x) for mod in mods) for QEFTLinear layers sharing the input x (..., ic); the
+    training path takes _QEFTGroupFn (summed dX in one buffer), inference on <= 16 tokens each
+    layer's decode GEMV."""
+    ic = mods[0].ic
+    if any(m.ic != ic or m.dl.tdtype != mods[0].dl.tdtype for m in mods) or x.shape[-1] != ic:
+        raise ShapeError("grouped_linear: layers must share the input width and dtype")
+    lead = x.shape[:-1]
+    x2 = x.reshape(-1, ic)
+    if x2.dtype != mods[0].dl.tdtype:
+        x2 = x2.to(mods[0].dl.tdtype)
+    grad = torch.is_grad_enabled() and (x2.requires_grad or any(m.weak32.requires_grad for m in mods))
+    if not grad and x2.shape[0] <= 16:
+        return [m(x) for m in mods]
+    ys = _QEFTGroupFn.apply(x2, tuple(mods), *[m.weak32 for m in mods])
+    return [y.reshape(*lead, m.oc) for y, m in zip(ys, mods)]
+
+
 _WEAK_VIEW = os.environ.get("QEFT_WEAK_VIEW", "1") != "0"  # A/B knob: 0 = always gather
 
 
