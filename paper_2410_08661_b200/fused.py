@@ -43,6 +43,40 @@ class _RMSNorm(torch.autograd.Function):
         return dx.view(dy.shape), None
 
 
+class _ResidualRMSNorm(torch.autograd.Function):
+    """(x, rms_norm(x)) for a residual stream x that both continues and feeds a norm: the
+    backward is ONE qeft_rmsnorm_bwd with the residual gradient folded in (its dres input),
+    instead of the norm's backward plus an autograd add."""
+
+    @staticmethod
+    def forward(ctx, x, gain):
+        C = x.shape[-1]
+        x2 = x.reshape(-1, C).contiguous()
+        y = torch.empty_like(x2)
+        rstd = torch.empty(x2.shape[0], dtype=torch.float32, device=x.device)
+        g = gain.float().contiguous()
+        _lib.check(_lib.lib().qeft_rmsnorm_fwd(x2.data_ptr(), g.data_ptr(), y.data_ptr(), rstd.data_ptr(),
+                                               x2.shape[0], C, _TDT[x.dtype], _lib.stream_ptr()), "rmsnorm_fwd")
+        ctx.save_for_backward(x2, g, rstd)
+        return x.view_as(x), y.view(x.shape)
+
+    @staticmethod
+    def backward(ctx, dres, dy):
+        x2, g, rstd = ctx.saved_tensors
+        C = x2.shape[1]
+        if dy is None:
+            return dres, None
+        dy2 = dy.reshape(-1, C).contiguous()
+        dr = dres.reshape(-1, C).contiguous() if dres is not None else None
+        if dr is not None and dr.dtype != dy2.dtype:
+            dr = dr.to(dy2.dtype)
+        dx = torch.empty_like(x2)
+        _lib.check(_lib.lib().qeft_rmsnorm_bwd(dy2.data_ptr(), x2.data_ptr(), g.data_ptr(), rstd.data_ptr(),
+                                               dr.data_ptr() if dr is not None else None, dx.data_ptr(),
+                                               x2.shape[0], C, _TDT[dy2.dtype], _lib.stream_ptr()), "rmsnorm_bwd")
+        return dx.view(dy.shape), None
+
+
 class _Rope(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, cos, sin, T, H, hd):
@@ -119,6 +153,11 @@ class _CrossEntropy(torch.autograd.Function):
 def cross_entropy(z, tgt):
     """mean_r(logsumexp(z[r]) - z[r, tgt[r]]) for fp16/bf16 CUDA logits (rows, V)."""
     return _CrossEntropy.apply(z, tgt)
+
+
+def residual_rms_norm(x, gain):
+    """(x, rms_norm(x, gain)): use the first output as the continuing residual stream."""
+    return _ResidualRMSNorm.apply(x, gain)
 
 
 def rms_norm(x, gain):

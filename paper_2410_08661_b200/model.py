@@ -87,7 +87,9 @@ class QEFTBlock(torch.nn.Module):
         """fp16/bf16 activations: RMS-norm, rotary and SwiGLU run as fused libqeft_b200 kernels."""
         B, T, _ = x.shape
         H, hd = cfg.n_heads, cfg.head_dim
-        a = fused.rms_norm(x, self.gain1)
+        # the residual stream passes through the norm's op, so its gradient joins the norm's
+        # backward kernel (no separate add)
+        x, a = fused.residual_rms_norm(x, self.gain1)
         # q/k/v (and gate/up) read the same normed input: one grouped op, whose backward sums
         # the three dX in one buffer (GEMM reduce-add epilogue)
         if _GROUPED:
@@ -99,7 +101,7 @@ class QEFTBlock(torch.nn.Module):
         v = vp.view(B, T, H, hd).transpose(1, 2)
         o = F.scaled_dot_product_attention(q, k, v, is_causal=True, scale=1.0 / math.sqrt(hd))
         x1 = x + self.wo(o.transpose(1, 2).reshape(B, T, H * hd))
-        b2 = fused.rms_norm(x1, self.gain2)
+        x1, b2 = fused.residual_rms_norm(x1, self.gain2)
         gt, up = grouped_linear([self.w_gate, self.w_up], b2) if _GROUPED else (self.w_gate(b2), self.w_up(b2))
         f = fused.silu_mul(gt, up)
         return x1 + self.w_down(f)
