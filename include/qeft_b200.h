@@ -184,6 +184,12 @@ int qeft_gemm_wgrad_weak(const qeft_linear_t* layer, const void* dy, int64_t ldd
                          int64_t ldxw, float* dw, int T, int accumulate, void* workspace,
                          size_t workspace_bytes, void* stream);
 
+/* dW_weak of up to 3 layers that read the same input (a block's q/k/v, gate/up) in one
+ * launch: dws[l] (+)= dys[l]^T x_weak, layers sharing k; dY row pitches 16-byte aligned. */
+int qeft_gemm_wgrad_weak_multi(const qeft_linear_t* const* layers, int n_layers, const void* const* dys,
+                               const int64_t* lddys, const void* x_weak, int64_t ldxw, float* const* dws, int T,
+                               int accumulate, void* stream);
+
 /* ---- optimizer (tuning.py:137-160 adam_step, tuning.py:226-236 clip) ---- */
 /* out[0] = sum(g^2) in fp64 (deterministic two-pass). scratch >= 4096 doubles. */
 int qeft_grad_sqnorm(const float* g, int64_t n, double* scratch, double* out, void* stream);

@@ -54,6 +54,7 @@ SIGNATURES = {
     "qeft_optq_codes": (_I, [_VP, _VP, _VP, _VP, _I, _I, _I, _I, _VP, _VP, _VP]),
     "qeft_gemv_trace": (_I, [_I, _VP]),
     "qeft_gemm_set_schedule": (_I, [_I, _I]),
+    "qeft_gemm_wgrad_weak_multi": (_I, [_VP, _I, _VP, _VP, _VP, _I64, _VP, _I, _I, _VP]),
     "qeft_gemv_multi_rmsnorm": (_I, [_VP, _I, _VP, _I64, _VP, _VP, _I64, _I, _I, _VP, _SZ, _VP]),
     "qeft_gemv_swiglu": (_I, [_LP, _VP, _VP, _I64, _VP, _I64, _I, _I, _VP, _SZ, _VP]),
     "qeft_gemv_workspace_bytes": (_SZ, [_LP, _I]),

@@ -138,6 +138,15 @@ size_t qeft_gemm_workspace_bytes(const qeft_linear_t* L, int T) { return gemm_wo
 
 int qeft_gemm_set_schedule(int what, int value) { return gemm_set_schedule(what, value); }
 
+int qeft_gemm_wgrad_weak_multi(const qeft_linear_t* const* Ls, int nl, const void* const* dys, const int64_t* lddys,
+                               const void* x_weak, int64_t ldxw, float* const* dws, int T, int accumulate, void* s) {
+  QEFT_CHECK(Ls != nullptr && dys != nullptr && dws != nullptr && lddys != nullptr, QEFT_ERR_SHAPE,
+             "wgrad_multi: null argument");
+  for (int l = 0; l < nl; ++l)
+    if (int r = check_layer(Ls[l])) return r;
+  return gemm_wgrad_weak_multi(Ls, nl, dys, lddys, x_weak, ldxw, dws, T, accumulate, ST(s));
+}
+
 int qeft_gemm_fwd(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_t ldy, int T,
                   void* ws, size_t wsb, void* s) {
   if (int r = check_layer(L)) return r;

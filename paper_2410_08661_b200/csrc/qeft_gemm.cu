@@ -940,10 +940,21 @@ struct WgradShape {
   static_assert((size_t)BM * kStride * 4 <= (size_t)kStages * (kSA + kSB), "staging fits the stages");
 };
 
+// Up to 3 layers that share the weak input columns (a block's q/k/v, or gate/up) in one
+// launch: blockIdx.y runs over all of their 128-channel blocks.
+constexpr int kMaxWgLayers = 3;
+struct WgradGroup {
+  CUtensorMap dy[kMaxWgLayers];
+  float* dw[kMaxWgLayers];
+  int oc[kMaxWgLayers];
+  int blk_end[kMaxWgLayers];  // cumulative channel blocks
+  int nl;
+};
+
 template <typename T, int NW>
 __global__ void __launch_bounds__(192, 1)
-wgrad_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_constant__ CUtensorMap map_xw,
-             float* __restrict__ dw, int oc, int k, int T_, int accumulate, int kb_split, int vec_out) {
+wgrad_kernel(const __grid_constant__ WgradGroup grp, const __grid_constant__ CUtensorMap map_xw, int k, int T_,
+             int accumulate, int kb_split, int vec_out) {
   using Sh = WgradShape<NW>;
   constexpr int N = Sh::N, kSA = Sh::kSA, kSB = Sh::kSB, kStages = Sh::kStages, kStride = Sh::kStride;
   constexpr int kCols = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
@@ -956,7 +967,12 @@ wgrad_kernel(const __grid_constant__ CUtensorMap map_dy, const __grid_constant__
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = gridDim.x, rank = blockIdx.x;  // cluster = the S token splits of one channel block
-  const int o0 = blockIdx.y * BM;
+  int l = 0;
+  while (l + 1 < grp.nl && (int)blockIdx.y >= grp.blk_end[l]) ++l;
+  const CUtensorMap& map_dy = grp.dy[l];
+  float* __restrict__ dw = grp.dw[l];
+  const int oc = grp.oc[l];
+  const int o0 = ((int)blockIdx.y - (l ? grp.blk_end[l - 1] : 0)) * BM;
   const int kb0 = rank * kb_split;
   const int nkb = max(0, min((T_ + 63) / 64 - kb0, kb_split));
   if (threadIdx.x == 0) {
@@ -1484,7 +1500,24 @@ int gemm_dgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, void* dx, i
 }
 
 template <typename T, int NW>
-int launch_wgrad(const CUtensorMap& md, const CUtensorMap& mx, float* dw, int oc, int k, int T_, int acc,
+int launch_wgrad(const WgradGroup& g, const CUtensorMap& mx, int k, int T_, int acc, int vec, cudaStream_t st);
+
+int dispatch_wgrad(const qeft_linear_t* L, const WgradGroup& g, const CUtensorMap& mx, int T_, int acc, int vec,
+                   cudaStream_t st) {
+  const int nw = L->k_pad / 64;
+  const bool bf = L->act_dtype == QEFT_BF16;
+#define QEFT_WG(NW)                                                                        \
+  if (nw == NW)                                                                            \
+    return bf ? launch_wgrad<__nv_bfloat16, NW>(g, mx, L->k, T_, acc, vec, st)              \
+              : launch_wgrad<__half, NW>(g, mx, L->k, T_, acc, vec, st);
+  QEFT_WG(1) QEFT_WG(2) QEFT_WG(3) QEFT_WG(4)
+#undef QEFT_WG
+  set_error("gemm_wgrad: unsupported k_pad");
+  return QEFT_ERR_LAYOUT;
+}
+
+template <typename T, int NW>
+int launch_wgrad(const WgradGroup& g, const CUtensorMap& mx, int k, int T_, int acc, int vec,
                  cudaStream_t st) {
   const size_t smem = WgradShape<NW>::kSmem;
   auto kern = wgrad_kernel<T, NW>;
@@ -1494,12 +1527,42 @@ int launch_wgrad(const CUtensorMap& md, const CUtensorMap& mx, float* dw, int oc
     attr = true;
   }
   const int nkb = (T_ + 63) / 64;
-  const int S = wgrad_splits(oc, T_);
+  const int blocks = g.blk_end[g.nl - 1];
+  const int S = wgrad_splits(blocks * BM, T_);
   const int kbs = (nkb + S - 1) / S;
-  const int vec = (k % 4 == 0) && (((uintptr_t)dw & 15) == 0);
-  QEFT_CUDA(launch_pdl_cluster(kern, dim3(S, (oc + BM - 1) / BM), dim3(192), smem, st, S, md, mx, dw, oc, k, T_,
-                               acc, kbs, vec));
+  QEFT_CUDA(launch_pdl_cluster(kern, dim3(S, blocks), dim3(192), smem, st, S, g, mx, k, T_, acc, kbs, vec));
   return 0;
+}
+
+int gemm_wgrad_weak_multi(const qeft_linear_t* const* Ls, int nl, const void* const* dys, const int64_t* lddys,
+                          const void* x_weak, int64_t ldxw, float* const* dws, int T_, int accumulate,
+                          cudaStream_t st) {
+  QEFT_CHECK(nl >= 1 && nl <= kMaxWgLayers && T_ >= 1, QEFT_ERR_SHAPE, "wgrad_multi: %d layers", nl);
+  const qeft_linear_t* L = Ls[0];
+  if (L->k == 0) return 0;
+  QEFT_CHECK(L->k_pad <= 256, QEFT_ERR_LAYOUT, "gemm_wgrad: k_pad=%d > 256", L->k_pad);
+  QEFT_CHECK(ldxw >= L->k && ldxw % 8 == 0 && ((uintptr_t)x_weak & 15) == 0, QEFT_ERR_SHAPE,
+             "wgrad_multi: x_weak needs a 16-byte aligned row pitch >= k");
+  WgradGroup g{};
+  g.nl = nl;
+  int vec = L->k % 4 == 0;
+  int blocks = 0;
+  for (int l = 0; l < nl; ++l) {
+    const qeft_linear_t* Li = Ls[l];
+    QEFT_CHECK(Li->k == L->k && Li->k_pad == L->k_pad && Li->act_dtype == L->act_dtype, QEFT_ERR_SHAPE,
+               "wgrad_multi: layer %d does not share the weak geometry", l);
+    QEFT_CHECK(lddys[l] >= Li->oc && lddys[l] % 8 == 0 && ((uintptr_t)dys[l] & 15) == 0, QEFT_ERR_SHAPE,
+               "wgrad_multi: dY of layer %d needs a 16-byte aligned row pitch", l);
+    if (int r = make_map(&g.dy[l], dys[l], Li->act_dtype, Li->oc, T_, lddys[l], 64)) return r;
+    g.dw[l] = dws[l];
+    g.oc[l] = Li->oc;
+    blocks += (Li->oc + BM - 1) / BM;
+    g.blk_end[l] = blocks;
+    vec = vec && (((uintptr_t)dws[l] & 15) == 0);
+  }
+  CUtensorMap mx;
+  if (int r = make_map(&mx, x_weak, L->act_dtype, L->k, T_, ldxw, 64)) return r;
+  return dispatch_wgrad(L, g, mx, T_, accumulate, vec, st);
 }
 
 int gemm_wgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, const void* x, int64_t ldx, float* dw,
@@ -1528,16 +1591,14 @@ int gemm_wgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, const void*
     if (int r = gather_rows(x, ldx, L->ic, L->colmap + L->m_pad, L->k_pad, T_, L->act_dtype, ws, st)) return r;
     if (int r = make_map(&mx, ws, L->act_dtype, L->k_pad, T_, L->k_pad, 64)) return r;
   }
-  const int nw = L->k_pad / 64;
-  const bool bf = L->act_dtype == QEFT_BF16;
-#define QEFT_WG(NW)                                                                              \
-  if (nw == NW)                                                                                  \
-    return bf ? launch_wgrad<__nv_bfloat16, NW>(md, mx, dw, L->oc, L->k, T_, accumulate, st) \
-              : launch_wgrad<__half, NW>(md, mx, dw, L->oc, L->k, T_, accumulate, st);
-  QEFT_WG(1) QEFT_WG(2) QEFT_WG(3) QEFT_WG(4)
-#undef QEFT_WG
-  set_error("gemm_wgrad: unsupported k_pad");
-  return QEFT_ERR_LAYOUT;
+  WgradGroup g{};
+  g.dy[0] = md;
+  g.dw[0] = dw;
+  g.oc[0] = L->oc;
+  g.blk_end[0] = (L->oc + BM - 1) / BM;
+  g.nl = 1;
+  const int vec = (L->k % 4 == 0) && (((uintptr_t)dw & 15) == 0);
+  return dispatch_wgrad(L, g, mx, T_, accumulate, vec, st);
 }
 
 }  // namespace qeft

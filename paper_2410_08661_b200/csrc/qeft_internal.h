@@ -74,6 +74,9 @@ int rmsnorm_fwd(const void* x, const float* gain, void* y, float* rstd, int rows
 
 size_t gemm_workspace_bytes(const qeft_linear_t* L, int T);
 int gemm_set_schedule(int what, int value);
+int gemm_wgrad_weak_multi(const qeft_linear_t* const* Ls, int nl, const void* const* dys, const int64_t* lddys,
+                          const void* x_weak, int64_t ldxw, float* const* dws, int T, int accumulate,
+                          cudaStream_t st);
 int cross_entropy_fwd(const void* z, int64_t ldz, int rows, int V, const int64_t* tgt, float* loss, float* lse,
                       int dt, cudaStream_t st);
 int cross_entropy_bwd(const void* z, int64_t ldz, int rows, int V, const int64_t* tgt, const float* lse,

@@ -17,6 +17,7 @@ is refreshed from the master after each optimizer step.
 
 from __future__ import annotations
 
+import ctypes
 import os
 
 import torch
@@ -81,6 +82,7 @@ class _QEFTGroupFn(torch.autograd.Function):
     def backward(ctx, *dys):
         xws = dict(zip(ctx.widx, ctx.saved_tensors))
         dx = None
+        wg = []  # (mod, dy, x_weak) of the layers with a trainable weak block
         for i, (mod, dy) in enumerate(zip(ctx.mods, dys)):
             if dy is None:
                 continue
@@ -91,10 +93,29 @@ class _QEFTGroupFn(torch.autograd.Function):
             if ctx.needs_input_grad[0]:
                 dx = dl.gemm_dgrad(dy) if dx is None else dl.gemm_dgrad(dy, out=dx, accumulate=True)
             if i in xws:
-                w = mod.weak32
-                if w.grad is None:
-                    w.grad = torch.zeros_like(w)
-                dl.gemm_wgrad_weak(dy, xws[i], out=w.grad, accumulate=True)
+                wg.append((mod, dy, xws[i]))
+        if wg:
+            for mod, _, _ in wg:
+                if mod.weak32.grad is None:
+                    mod.weak32.grad = torch.zeros_like(mod.weak32)
+            xw = wg[0][2]
+            same = all(w[2].data_ptr() == xw.data_ptr() and w[0].dl.k == wg[0][0].dl.k for w in wg)
+            if len(wg) > 1 and same and all(w[1].stride(0) % 8 == 0 for w in wg) and xw.stride(0) % 8 == 0:
+                # every dW_weak of the group in one launch (they share the weak input columns)
+                L = _lib.lib()
+                n = len(wg)
+                arr = (ctypes.POINTER(_lib.QeftLinearT) * n)(*[w[0].dl.cptr for w in wg])
+                dyp = (ctypes.c_void_p * n)(*[w[1].data_ptr() for w in wg])
+                ldd = (ctypes.c_int64 * n)(*[w[1].stride(0) for w in wg])
+                dwp = (ctypes.c_void_p * n)(*[w[0].weak32.grad.data_ptr() for w in wg])
+                _lib.check(L.qeft_gemm_wgrad_weak_multi(ctypes.cast(arr, ctypes.c_void_p), n, ctypes.cast(dyp, ctypes.c_void_p),
+                                                        ctypes.cast(ldd, ctypes.c_void_p), xw.data_ptr(), xw.stride(0),
+                                                        ctypes.cast(dwp, ctypes.c_void_p), wg[0][1].shape[0], 1,
+                                                        _lib.stream_ptr()), "gemm_wgrad_weak_multi")
+            else:
+                for mod, dy, x_w in wg:
+                    mod.dl.gemm_wgrad_weak(dy, x_w, out=mod.weak32.grad, accumulate=True)
+            for mod, _, _ in wg:
                 if mod.grad_ready_hook is not None:
                     mod.grad_ready_hook(mod)
         return (dx, None) + (None,) * len(ctx.mods)

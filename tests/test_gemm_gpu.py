@@ -201,3 +201,31 @@ def test_cta_pairs_match_single(Q, case, sk):
     assert rel_err(dx2a.float().cpu().numpy(), 2 * dref.cpu().numpy()) <= TOL
     assert rel_err(y2.float().cpu().numpy(), y1.float().cpu().numpy()) <= _ulp2(dt)
     assert rel_err(dx2.float().cpu().numpy(), dx1.float().cpu().numpy()) <= _ulp2(dt)
+
+
+def test_wgrad_weak_multi_matches_per_layer(Q):
+    """qeft_gemm_wgrad_weak_multi (q/k/v-style layers sharing the weak input columns, one launch)
+    equals one qeft_gemm_wgrad_weak per layer (the token split may differ: fp32 sums to 1e-5)."""
+    import ctypes
+    import torch
+    from paper_2410_08661_b200 import _lib
+    from paper_2410_08661_b200.decode import random_layer
+    T = 1000
+    dls = [random_layer(oc, 1024, 128, 4, 128, "f16", seed=s) for s, oc in enumerate((512, 384, 512))]
+    x = torch.randn(T, 1024, device="cuda").half()
+    xw = x[:, dls[0].m:dls[0].m + dls[0].k]
+    dys = [torch.randn(T, dl.oc, device="cuda").half() for dl in dls]
+    ref = [dl.gemm_wgrad_weak(dy, xw) for dl, dy in zip(dls, dys)]
+    out = [torch.full_like(r, 0.5) for r in ref]
+    L = _lib.lib()
+    n = len(dls)
+    arr = (ctypes.POINTER(_lib.QeftLinearT) * n)(*[d.cptr for d in dls])
+    dyp = (ctypes.c_void_p * n)(*[d.data_ptr() for d in dys])
+    ldd = (ctypes.c_int64 * n)(*[d.stride(0) for d in dys])
+    dwp = (ctypes.c_void_p * n)(*[o.data_ptr() for o in out])
+    _lib.check(L.qeft_gemm_wgrad_weak_multi(ctypes.cast(arr, ctypes.c_void_p), n, ctypes.cast(dyp, ctypes.c_void_p),
+                                            ctypes.cast(ldd, ctypes.c_void_p), xw.data_ptr(), xw.stride(0),
+                                            ctypes.cast(dwp, ctypes.c_void_p), T, 1, _lib.stream_ptr()), "multi")
+    torch.cuda.synchronize()
+    for r, o in zip(ref, out):
+        assert rel_err((o - 0.5).cpu().numpy(), r.cpu().numpy()) <= 1e-5
