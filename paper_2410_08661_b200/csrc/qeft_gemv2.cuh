@@ -130,7 +130,10 @@ QEFT_DEV uint2 lds64(const void* p) { return *reinterpret_cast<const uint2*>(p);
 // Launch shape (template): NW warps per CTA, CPS 128-column chunks per codes stage (a stage
 // holds CPS KB of 4-bit codes + their sz16 pairs, or CPS / 2 weak tiles), R stages per ring.
 // ONE: a single activation column (batch-1 decode): only column 0 of the MMA output is live.
-template <int BITS, int NT, int GT, typename T, int R, int NW, int CPS, bool ONE, int MINB, int PRE, bool CONTIG>
+// FUSED: the decode step's RMS-norm / SwiGLU in the x staging (separate instantiations, so the
+// plain kernel carries none of it)
+template <int BITS, int NT, int GT, typename T, int R, int NW, int CPS, bool ONE, int MINB, int PRE, bool CONTIG,
+          bool FUSED = false>
 __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
   constexpr int kWPS = CPS / 2;
   constexpr int kSzOff = CPS * 1024, kStage = CPS * 1152;  // codes, then sz16 pairs
@@ -248,13 +251,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
         if (bytes) {
           T* xus = reinterpret_cast<T*>(smem + a.xu_off);
           const T* xu = reinterpret_cast<const T*>(a.xu);
-          mbar_expect_tx(&xbar, a.xu ? 2 * bytes : bytes);
+          mbar_expect_tx(&xbar, (FUSED && a.xu) ? 2 * bytes : bytes);
           for (int r = 0; r < n; ++r) {
             if (q1 > kb) bulk_g2s(xs + r * a.xs_ld, x + r * a.ldx + kb, (uint32_t)(q1 - kb) * 2u, &xbar);
             if (w_end > w_beg)
               bulk_g2s(xs + r * a.xs_ld + (w_beg - kb), x + r * a.ldx + a.m + (w_beg - a.m_pad),
                        (uint32_t)(w_end - w_beg) * 2u, &xbar);
-            if (a.xu) {
+            if (FUSED && a.xu) {
               if (q1 > kb) bulk_g2s(xus + r * a.xs_ld, xu + r * a.ldx + kb, (uint32_t)(q1 - kb) * 2u, &xbar);
               if (w_end > w_beg)
                 bulk_g2s(xus + r * a.xs_ld + (w_beg - kb), xu + r * a.ldx + a.m + (w_beg - a.m_pad),
@@ -278,7 +281,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
         xs[r * a.xs_ld + (c < nz0 ? z0a + c : z1a + c - nz0) - kb] = zero;
       }
       mbar_wait(&xbar, 0);
-      if (a.xu) {
+      if (FUSED && a.xu) {
         // SwiGLU in place, the stand-alone kernel's expression (bit-identical): x = silu(g) * u
         const T* xus = reinterpret_cast<const T*>(smem + a.xu_off);
         const int nq = max(q1 - kb, 0), nw = max(w_end - w_beg, 0);
@@ -355,7 +358,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
     }
   }
   __syncthreads();
-  if (a.ngain) {
+  if (FUSED && a.ngain) {
     // fused RMS-norm of the staged x, bit-identical to qeft_rmsnorm_fwd: the first nthr threads
     // sum x^2 in that kernel's order (8 consecutive columns per thread, stride nthr * 8, warp
     // shuffles, then across warps), read from the staged row when it holds every column
@@ -739,6 +742,24 @@ int launch2(G2Args a, cudaStream_t st) {
   auto kernN = gemv2_kernel<BITS, NT, GT, T, R, NW, CPS, false, MINB, PRE, CONTIG>;
   const bool one = a.n == 1 && NT == 1;
   auto kern = one ? kern1 : kernN;
+  const bool fused = a.ngain || a.xu;
+  if constexpr (NT == 1 && NW == 16 && CPS == 4 && !CONTIG && MINB == 1) {
+    if (fused) {
+      static bool fattr = false;
+      auto f1 = gemv2_kernel<BITS, NT, GT, T, R, NW, CPS, true, MINB, PRE, CONTIG, true>;
+      auto fN = gemv2_kernel<BITS, NT, GT, T, R, NW, CPS, false, MINB, PRE, CONTIG, true>;
+      if (!fattr) {
+        for (auto kk : {f1, fN}) {
+          QEFT_CUDA(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+          QEFT_CUDA(cudaFuncSetAttribute(kk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        }
+        fattr = true;
+      }
+      kern = one ? f1 : fN;
+    }
+  } else {
+    if (fused) return -1;  // the decode plans host the fusions; others use the stand-alone kernels
+  }
   static bool attr = false;
   if (!attr) {
     for (auto kk : {kern1, kernN}) {
