@@ -242,6 +242,15 @@ int qeft_rmsnorm_bwd(const void* dy, const void* x, const float* gain, const flo
 int qeft_rope_kv(const void* q, const void* k, const void* v, void* q_out, void* k_cache, void* v_cache,
                  const float* cos_t, const float* sin_t, const int64_t* pos, int B, int H, int hd, int T_cache, int dt,
                  void* stream);
+/* Decode step attention with the rotary + cache append fused in: q, k, v (B, H*hd) of the new
+ * token; k rotated and k/v written to the caches (B, H, T_cache, hd) at *pos (device int64);
+ * o (B, H*hd) = softmax(rot(q) . K[0..pos]^T / sqrt(hd)) V[0..pos], fp32 softmax; hd = 128. */
+size_t qeft_decode_attention_workspace_bytes(int B, int H, int hd);
+/* workspace: qeft_decode_attention_workspace_bytes(), zero-filled once (its counters are left at
+ * zero by every call), one per stream. */
+int qeft_decode_attention(const void* q, const void* k, const void* v, void* k_cache, void* v_cache,
+                          const float* cos_t, const float* sin_t, const int64_t* pos, void* o, int B, int H, int hd,
+                          int T_cache, int dt, void* workspace, size_t workspace_bytes, void* stream);
 int qeft_rope(const void* in, void* out, const float* cos_t, const float* sin_t, int64_t rows, int T, int H,
               int hd, int inverse, int dt, void* stream);
 int qeft_silu_mul_fwd(const void* g, const void* u, void* f, int64_t n, int dt, void* stream);

@@ -78,6 +78,8 @@ SIGNATURES = {
     "qeft_rope": (_I, [_VP, _VP, _VP, _VP, _I64, _I, _I, _I, _I, _I, _VP]),
     "qeft_rope_kv": (_I, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I, _I, _I, _I, _I, _VP]),
     "qeft_silu_mul_fwd": (_I, [_VP, _VP, _VP, _I64, _I, _VP]),
+    "qeft_decode_attention": (_I, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I, _I, _I, _I, _I, _VP, _SZ, _VP]),
+    "qeft_decode_attention_workspace_bytes": (_SZ, [_I, _I, _I]),
     "qeft_cross_entropy_fwd": (_I, [_VP, _I64, _I, _I, _VP, _VP, _VP, _I, _VP]),
     "qeft_cross_entropy_bwd": (_I, [_VP, _I64, _I, _I, _VP, _VP, _VP, _VP, _I64, _I, _VP]),
     "qeft_silu_mul_bwd": (_I, [_VP, _VP, _VP, _VP, _VP, _I64, _I, _VP]),

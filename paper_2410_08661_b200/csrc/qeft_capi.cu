@@ -221,6 +221,14 @@ int qeft_rope(const void* in, void* out, const float* cosv, const float* sinv, i
   return rope(in, out, cosv, sinv, rows, T, H, hd, inverse, dt, ST(s));
 }
 
+size_t qeft_decode_attention_workspace_bytes(int B, int H, int hd) { return decode_attention_workspace_bytes(B, H, hd); }
+
+int qeft_decode_attention(const void* q, const void* k, const void* v, void* kc, void* vc, const float* cos_t,
+                          const float* sin_t, const int64_t* pos, void* o, int B, int H, int hd, int T_cache, int dt,
+                          void* ws, size_t ws_bytes, void* s) {
+  return decode_attention(q, k, v, kc, vc, cos_t, sin_t, pos, o, B, H, hd, T_cache, dt, ws, ws_bytes, ST(s));
+}
+
 int qeft_cross_entropy_fwd(const void* z, int64_t ldz, int rows, int V, const int64_t* tgt, float* loss,
                            float* lse, int dt, void* s) {
   return cross_entropy_fwd(z, ldz, rows, V, tgt, loss, lse, dt, ST(s));

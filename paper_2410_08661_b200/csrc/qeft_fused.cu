@@ -183,6 +183,170 @@ __global__ void rope_kv_kernel(const T* __restrict__ q, const T* __restrict__ k,
   }
 }
 
+// One decode step's attention, with the rotary + KV-cache append fused in (model.py:249-275
+// rotary, the engine's causal softmax attention): grid (head, batch, split). Every CTA rotates q
+// at the device position; the split holding position pos also rotates the new k and appends
+// k/v to the caches. Each split attends to its contiguous chunk of positions 0..pos with an
+// fp32 online softmax: half-warps own positions (16 lanes x 8 dims, 16-byte loads), K and V of
+// UNR positions are loaded together, the 32 half-warp states are merged in shared memory, and
+// the split's (max, sum, o) goes to the scratch; the last split to finish (a per-head counter)
+// merges the splits in split order (deterministic), writes o and re-arms the counter.
+constexpr int kAttnSplits = 4;
+
+template <typename T, int HD>
+__global__ void __launch_bounds__(512) decode_attn_kernel(const T* __restrict__ q, const T* __restrict__ k,
+                                                          const T* __restrict__ v, T* __restrict__ kc,
+                                                          T* __restrict__ vc, const float* __restrict__ cosv,
+                                                          const float* __restrict__ sinv,
+                                                          const int64_t* __restrict__ pos_dev, T* __restrict__ o,
+                                                          float* __restrict__ scratch, int* __restrict__ counters,
+                                                          int H, int T_cache, float scale) {
+  constexpr int DPL = HD / 16;  // dims per lane of a half-warp
+  constexpr int HALF = HD / 2;
+  constexpr int UNR = 8;
+  constexpr int NHW = 512 / 16;  // half-warps
+  constexpr int PART = HD + 2;   // scratch floats per split: o[HD], max, sum
+  static_assert(DPL == 8, "16-byte lanes: HD = 128");
+  __shared__ __align__(16) T qs[HD];
+  __shared__ float s_m[NHW], s_l[NHW];
+  __shared__ __align__(16) float s_o[NHW][HD];
+  __shared__ int s_last;
+  const int h = blockIdx.x, b = blockIdx.y, split = blockIdx.z, S = gridDim.z;
+  const int pos = (int)*pos_dev;
+  const int n = pos + 1;
+  const int c0 = (int)((int64_t)split * n / S), c1 = (int)((int64_t)(split + 1) * n / S);
+  const int64_t src = ((int64_t)b * H + h) * HD;
+  const int64_t crow = ((int64_t)b * H + h) * T_cache;
+  const int hw = threadIdx.x >> 4, l16 = threadIdx.x & 15;
+  const T* kbase = kc + crow * HD + l16 * DPL;
+  const T* vbase = vc + crow * HD + l16 * DPL;
+  // before the grid dependency: the rotary constants and the first UNR cached rows of this
+  // half-warp (rows < pos were written by earlier steps; row pos is appended below)
+  float cs = 0.f, sn = 0.f;
+  if (threadIdx.x < HALF) {
+    cs = cosv[(int64_t)pos * HALF + threadIdx.x];
+    sn = sinv[(int64_t)pos * HALF + threadIdx.x];
+  }
+  uint4 kv[UNR], vv[UNR];
+  const int t00 = c0 + (hw & ~1);
+#pragma unroll
+  for (int u = 0; u < UNR; ++u) {
+    const int t = t00 + (hw & 1) + u * NHW;
+    kv[u] = make_uint4(0u, 0u, 0u, 0u);
+    vv[u] = kv[u];
+    if (t < c1 && t < pos) {
+      kv[u] = __ldcg(reinterpret_cast<const uint4*>(kbase + (int64_t)t * HD));
+      vv[u] = __ldcg(reinterpret_cast<const uint4*>(vbase + (int64_t)t * HD));
+    }
+  }
+  pdl_launch_dependents();
+  pdl_wait();  // q / k / v come from the preceding projection
+  if (threadIdx.x < HALF) {
+    const int j = threadIdx.x;
+    const float c = cs, s = sn;
+    float a = to_f32<T>(q[src + j]), bb = to_f32<T>(q[src + j + HALF]);
+    qs[j] = from_f32<T>(a * c - bb * s);
+    qs[j + HALF] = from_f32<T>(a * s + bb * c);
+    if (c1 == n) {  // this split's chunk ends at pos: append the new row
+      a = to_f32<T>(k[src + j]);
+      bb = to_f32<T>(k[src + j + HALF]);
+      kc[(crow + pos) * HD + j] = from_f32<T>(a * c - bb * s);
+      kc[(crow + pos) * HD + j + HALF] = from_f32<T>(a * s + bb * c);
+      vc[(crow + pos) * HD + j] = v[src + j];
+      vc[(crow + pos) * HD + j + HALF] = v[src + j + HALF];
+    }
+  }
+  __syncthreads();  // rotated q in shared memory, the new cache row written (same CTA)
+  float qf[DPL];
+  {
+    const uint4 qv = *reinterpret_cast<const uint4*>(qs + l16 * DPL);
+    const T* e = reinterpret_cast<const T*>(&qv);
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) qf[i] = to_f32<T>(e[i]);
+  }
+  float m = -INFINITY, lsum = 0.f, acc[DPL];
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
+  // warp-uniform trip count (the even half-warp's positions); the odd half masks its tail
+  for (int t0 = t00; t0 < c1; t0 += NHW * UNR) {
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int t = t0 + (hw & 1) + u * NHW;
+      // the first iteration's rows were prefetched, except the one appended above
+      if (t < c1 && (t0 != t00 || t >= pos)) {
+        kv[u] = __ldcg(reinterpret_cast<const uint4*>(kbase + (int64_t)t * HD));
+        vv[u] = __ldcg(reinterpret_cast<const uint4*>(vbase + (int64_t)t * HD));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int t = t0 + (hw & 1) + u * NHW;
+      const T* ke = reinterpret_cast<const T*>(&kv[u]);
+      float d = 0.f;
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) d = fmaf(qf[i], to_f32<T>(ke[i]), d);
+#pragma unroll
+      for (int off = 8; off >= 1; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
+      if (t < c1) {
+        const float sc = d * scale;
+        const float mn = fmaxf(m, sc);
+        const float corr = __expf(m - mn), p = __expf(sc - mn);
+        lsum = lsum * corr + p;
+        const T* ve = reinterpret_cast<const T*>(&vv[u]);
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) acc[i] = fmaf(p, to_f32<T>(ve[i]), acc[i] * corr);
+        m = mn;
+      }
+    }
+  }
+  if (l16 == 0) {
+    s_m[hw] = m;
+    s_l[hw] = lsum;
+  }
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) s_o[hw][l16 * DPL + i] = acc[i];
+  __syncthreads();
+  // this split's state: merge the half-warps in order
+  float* part = scratch + (((int64_t)b * H + h) * S + split) * PART;
+  if (threadIdx.x < HD) {
+    float M = -INFINITY;
+    for (int w = 0; w < NHW; ++w) M = fmaxf(M, s_m[w]);
+    float L = 0.f, O = 0.f;
+    for (int w = 0; w < NHW; ++w) {
+      if (s_m[w] == -INFINITY) continue;  // a half-warp with no position
+      const float f = __expf(s_m[w] - M);
+      L += s_l[w] * f;
+      O += s_o[w][threadIdx.x] * f;
+    }
+    part[threadIdx.x] = O;
+    if (threadIdx.x == 0) {
+      part[HD] = M;
+      part[HD + 1] = L;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(counters + (int64_t)b * H + h, 1) == S - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x < HD) {
+    const float* p0 = scratch + ((int64_t)b * H + h) * S * PART;
+    float M = -INFINITY;
+    for (int sp = 0; sp < S; ++sp) M = fmaxf(M, __ldcg(p0 + sp * PART + HD));
+    float L = 0.f, O = 0.f;
+    for (int sp = 0; sp < S; ++sp) {
+      const float ms = __ldcg(p0 + sp * PART + HD);
+      if (ms == -INFINITY) continue;  // an empty split
+      const float f = __expf(ms - M);
+      L += __ldcg(p0 + sp * PART + HD + 1) * f;
+      O += __ldcg(p0 + sp * PART + threadIdx.x) * f;
+    }
+    o[src + threadIdx.x] = from_f32<T>(O / L);
+  }
+  if (threadIdx.x == 0) counters[(int64_t)b * H + h] = 0;
+}
+
 // f = silu(g) * u (SwiGLU, model.py:389-391) and its backward
 template <typename T>
 __global__ void silu_mul_fwd_kernel(const T* __restrict__ g, const T* __restrict__ u, T* __restrict__ f, int64_t n) {
@@ -364,6 +528,34 @@ int rope_kv(const void* q, const void* k, const void* v, void* q_out, void* kc, 
   else
     rope_kv_kernel<__half><<<B, thr, 0, st>>>((const __half*)q, (const __half*)k, (const __half*)v, (__half*)q_out,
                                               (__half*)kc, (__half*)vc, cosv, sinv, pos_dev, H, hd, T_cache);
+  QEFT_CUDA(cudaGetLastError());
+  return 0;
+}
+
+size_t decode_attention_workspace_bytes(int B, int H, int hd) {
+  // counters [B*H] (zero between calls; the kernel re-arms them), then the split partials
+  return 256 + (((size_t)B * H * 4 + 63) & ~(size_t)63) + (size_t)B * H * kAttnSplits * (hd + 2) * 4;
+}
+
+int decode_attention(const void* q, const void* k, const void* v, void* kc, void* vc, const float* cosv,
+                     const float* sinv, const int64_t* pos_dev, void* o, int B, int H, int hd, int T_cache, int dt,
+                     void* ws, size_t ws_bytes, cudaStream_t st) {
+  QEFT_CHECK(hd == 128 && B >= 1 && H >= 1 && T_cache >= 1, QEFT_ERR_SHAPE,
+             "decode_attention: hd=%d (128 supported), B=%d H=%d T=%d", hd, B, H, T_cache);
+  QEFT_CHECK(ws != nullptr && ws_bytes >= decode_attention_workspace_bytes(B, H, hd) && ((uintptr_t)ws & 15) == 0,
+             QEFT_ERR_SHAPE, "decode_attention: workspace too small");
+  int* counters = (int*)ws;
+  float* scratch = (float*)((char*)ws + 256 + (((size_t)B * H * 4 + 63) & ~(size_t)63));
+  const float scale = 1.f / sqrtf((float)hd);
+  const dim3 grid(H, B, kAttnSplits);
+  if (dt == QEFT_BF16)
+    QEFT_CUDA(launch_pdl(decode_attn_kernel<__nv_bfloat16, 128>, grid, dim3(512), 0, st, (const __nv_bfloat16*)q,
+                         (const __nv_bfloat16*)k, (const __nv_bfloat16*)v, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, cosv,
+                         sinv, pos_dev, (__nv_bfloat16*)o, scratch, counters, H, T_cache, scale));
+  else
+    QEFT_CUDA(launch_pdl(decode_attn_kernel<__half, 128>, grid, dim3(512), 0, st, (const __half*)q, (const __half*)k,
+                         (const __half*)v, (__half*)kc, (__half*)vc, cosv, sinv, pos_dev, (__half*)o, scratch,
+                         counters, H, T_cache, scale));
   QEFT_CUDA(cudaGetLastError());
   return 0;
 }

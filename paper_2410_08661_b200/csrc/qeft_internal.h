@@ -74,6 +74,10 @@ int rmsnorm_fwd(const void* x, const float* gain, void* y, float* rstd, int rows
 
 size_t gemm_workspace_bytes(const qeft_linear_t* L, int T);
 int gemm_set_schedule(int what, int value);
+size_t decode_attention_workspace_bytes(int B, int H, int hd);
+int decode_attention(const void* q, const void* k, const void* v, void* kc, void* vc, const float* cosv,
+                     const float* sinv, const int64_t* pos_dev, void* o, int B, int H, int hd, int T_cache, int dt,
+                     void* ws, size_t ws_bytes, cudaStream_t st);
 int gemm_wgrad_weak_multi(const qeft_linear_t* const* Ls, int nl, const void* const* dys, const int64_t* lddys,
                           const void* x_weak, int64_t ldxw, float* const* dws, int T, int accumulate,
                           cudaStream_t st);

@@ -173,6 +173,27 @@ def silu_mul(g, u):
     return _SiluMul.apply(g, u)
 
 
+def decode_attention(q, k, v, k_cache, v_cache, cos, sin, pos_dev, H, hd, out=None):
+    """Decode step (no autograd): rotary on q/k at *pos_dev, k/v appended to the caches, and the
+    query's causal attention over positions 0..pos in one kernel; returns o (B, H*hd)."""
+    from .layer import _Workspace
+    global _ATTN_WS
+    B, T = q.shape[0], k_cache.shape[2]
+    o = torch.empty_like(q) if out is None else out
+    L = _lib.lib()
+    if _ATTN_WS is None:
+        _ATTN_WS = _Workspace()  # zero-filled once per (device, stream); the kernel re-arms its counters
+    ws = _ATTN_WS.get(int(L.qeft_decode_attention_workspace_bytes(B, H, hd)), q.device)
+    _lib.check(L.qeft_decode_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), k_cache.data_ptr(),
+                                       v_cache.data_ptr(), cos.data_ptr(), sin.data_ptr(), pos_dev.data_ptr(),
+                                       o.data_ptr(), B, H, hd, T, _TDT[q.dtype], ws.data_ptr(), ws.numel(),
+                                       _lib.stream_ptr()), "decode_attention")
+    return o
+
+
+_ATTN_WS = None
+
+
 def rope_kv(q, k, v, q_out, k_cache, v_cache, cos, sin, pos_dev, H, hd):
     """Decode step (no autograd): q_out = rope(q); k_cache/v_cache[:, :, *pos_dev] = rope(k), v.
     q/k/v (B, H*hd); caches (B, H, T, hd); pos_dev a device int64 scalar."""

@@ -5,8 +5,8 @@ each new token recomputes the whole prefix, every linear layer going column by c
 its matvec path. `KVDecoder` is the B200 form of the same greedy loop. Per token and block it runs:
   q/k/v: one qeft_gemv_multi_rmsnorm launch when the three share geometry (the RMS-norm runs
      in its x staging), else RMS-norm + per-layer qeft_gemv
-  -> rotary on q/k at the token's position + k/v appended to the cache (one qeft_rope_kv)
-  -> attention over the cache (torch SDPA, fp32 softmax inside the kernel)
+  -> rotary on q/k at the token's position + k/v appended to the cache + attention over
+     positions 0..pos, fp32 softmax (one qeft_decode_attention; rope_kv + torch SDPA otherwise)
   -> o (qeft_gemv, irregular / online-reorder layouts gather x in-kernel), the residual add
      fused into its epilogue (QEFT_Y_ACCUMULATE)
   -> gate/up (one launch, RMS-norm in its x staging) -> down over silu(gate)*up (SwiGLU in its
@@ -82,7 +82,7 @@ class KVDecoder:
         H, hd = cfg.n_heads, cfg.head_dim
         dyn = isinstance(pos, torch.Tensor)
         x = F.embedding(tok, self.emb).contiguous()  # (B, d) residual stream, updated in place
-        if dyn:
+        if dyn and hd != 128:
             # additive mask (0 / -inf) built once per step: a boolean mask would be converted
             # (fill + masked_fill) inside every block's attention call
             keep = torch.zeros(1, 1, 1, self.T, dtype=self.dt, device=tok.device).masked_fill_(
@@ -97,16 +97,21 @@ class KVDecoder:
                 a = fused.rms_norm(x, blk.gain1)
                 q, k, v = blk.wq.dl.gemv(a), blk.wk.dl.gemv(a), blk.wv.dl.gemv(a)
             kc, vc = self.k_cache[i], self.v_cache[i]
-            # rotary on q and k + the cache append at the device position, one kernel
-            qr = fused.rope_kv(q, k, v, torch.empty_like(q), kc, vc, self.cos, self.sin, self.pos_dev, H, hd)
-            q = qr.view(B, H, 1, hd)
-            if dyn:
-                o = F.scaled_dot_product_attention(q, kc, vc, attn_mask=keep, scale=1.0 / math.sqrt(hd))
+            if dyn and hd == 128:
+                # rotary + cache append + attention over positions 0..pos, one kernel
+                o2 = fused.decode_attention(q, k, v, kc, vc, self.cos, self.sin, self.pos_dev, H, hd)
             else:
-                o = F.scaled_dot_product_attention(q, kc[:, :, :pos + 1], vc[:, :, :pos + 1],
-                                                   scale=1.0 / math.sqrt(hd))
+                # rotary on q and k + the cache append at the device position, one kernel
+                qr = fused.rope_kv(q, k, v, torch.empty_like(q), kc, vc, self.cos, self.sin, self.pos_dev, H, hd)
+                qh = qr.view(B, H, 1, hd)
+                if dyn:
+                    o = F.scaled_dot_product_attention(qh, kc, vc, attn_mask=keep, scale=1.0 / math.sqrt(hd))
+                else:
+                    o = F.scaled_dot_product_attention(qh, kc[:, :, :pos + 1], vc[:, :, :pos + 1],
+                                                       scale=1.0 / math.sqrt(hd))
+                o2 = o.transpose(1, 2).reshape(B, H * hd)
             x = x.contiguous()
-            blk.wo.dl.gemv(o.transpose(1, 2).reshape(B, H * hd), out=x, accumulate=True)  # x += Wo o
+            blk.wo.dl.gemv(o2, out=x, accumulate=True)  # x += Wo o
             if self.gu_fused[i]:
                 gt = torch.empty(B, blk.w_gate.oc, dtype=self.dt, device=x.device)
                 up = torch.empty_like(gt)

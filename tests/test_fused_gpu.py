@@ -125,3 +125,34 @@ def test_cross_entropy_matches_fp32_torch(dt, rows, V):
     ulp = 2.0 ** -10 if dt == "f16" else 2.0 ** -7
     err = (z.grad.float() - zr.grad.to(td).float()).abs().max()
     assert float(err) <= ulp * float(zr.grad.abs().max()) + 1e-7
+
+
+@pytest.mark.parametrize("dt,B,pos", [("f16", 1, 0), ("f16", 1, 600), ("bf16", 2, 77)])
+def test_decode_attention_matches_rope_kv_sdpa(dt, B, pos):
+    """qeft_decode_attention (rotary + cache append + causal attention over 0..pos, one kernel)
+    against qeft_rope_kv + torch SDPA on a copy of the same caches: identical cache rows, and
+    the output within one fp16/bf16 rounding of the fp32 softmax attention."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2410_08661_b200 import fused
+    from paper_2410_08661_b200.model import rope_tables
+    td = torch.float16 if dt == "f16" else torch.bfloat16
+    H, hd, T = 32, 128, 641
+    g = torch.Generator(device="cuda").manual_seed(pos + B)
+    q, k, v = [(torch.randn(B, H * hd, device="cuda", generator=g)).to(td) for _ in range(3)]
+    kc = (torch.randn(B, H, T, hd, device="cuda", generator=g)).to(td)
+    vc = (torch.randn(B, H, T, hd, device="cuda", generator=g)).to(td)
+    kc2, vc2 = kc.clone(), vc.clone()
+    cos, sin = rope_tables(hd, T, "cuda")
+    p = torch.tensor(pos, dtype=torch.int64, device="cuda")
+    o = fused.decode_attention(q, k, v, kc, vc, cos, sin, p, H, hd)
+    qr = fused.rope_kv(q, k, v, torch.empty_like(q), kc2, vc2, cos, sin, p, H, hd)
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        qr.view(B, H, 1, hd).float(), kc2[:, :, :pos + 1].float(), vc2[:, :, :pos + 1].float(),
+        scale=1.0 / math.sqrt(hd)).transpose(1, 2).reshape(B, H * hd)
+    torch.cuda.synchronize()
+    assert torch.equal(kc, kc2) and torch.equal(vc, vc2)
+    ulp = 2.0 ** -10 if dt == "f16" else 2.0 ** -7
+    err = (o.float() - ref).abs().max()
+    assert float(err) <= 2 * ulp * float(ref.abs().max()) + 1e-3, float(err)
