@@ -881,21 +881,6 @@ int launch2(G2Args a, cudaStream_t st) {
 template <int BITS, typename T>
 int dispatch2(const G2Args& a, int gt, cudaStream_t st) {
   const bool nt2 = a.n > 8;
-  if constexpr (BITS == 4 && std::is_same<T, __half>::value) {
-    // tuning variants of the 7B decode path (4-bit, g = 128, <= 8 columns)
-    static const int var = env_int("QEFT_GEMV2_VAR", 0);
-    if (!nt2 && gt == 2 && var) {
-      switch (var) {
-        case 1: return launch2<4, 1, 2, T, 3, 8, 4>(a, st);
-        case 2: return launch2<4, 1, 2, T, 2, 8, 8>(a, st);
-        case 3: return launch2<4, 1, 2, T, 2, 12, 4>(a, st);
-        case 4: return launch2<4, 1, 2, T, 2, 8, 4, false, 2>(a, st);
-        case 5: return launch2<4, 1, 2, T, 2, 16, 4, false, 1>(a, st);
-        case 6: return launch2<4, 1, 2, T, 2, 8, 4, false, 2, 1>(a, st);
-        default: break;
-      }
-    }
-  }
   // launch2 returns -1 when the plan does not fit shared memory: try the next shape
 #define QEFT_G2(CONTIG, NT, NWV, CPSV)                                                   \
   {                                                                                      \
