@@ -1312,7 +1312,7 @@ int launch_gemm(const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap&
 struct GemmPlan {
   int bn, nsub, cg;
 };
-GemmPlan gemm_plan(int n_mblk, int T_) {
+GemmPlan gemm_plan(int n_mblk, int T_, int n_kblk) {
   // tile N: 128 tokens (T <= 128), 256, or 2 x 256 sharing each dequantized A stage (T > 256;
   // QEFT_GEMM_NSUB=1 forces single sub-tiles)
   static const int nsub_env = getenv("QEFT_GEMM_NSUB") ? atoi(getenv("QEFT_GEMM_NSUB")) : 0;
@@ -1321,7 +1321,10 @@ GemmPlan gemm_plan(int n_mblk, int T_) {
   // paired sub-tiles halve dequant work per FLOP, but when even twice the items of single
   // sub-tiles fit one wave (few m-blocks, short T: 13B T=512), parallelism wins
   const int pair_items = n_mblk * ((T_ + 511) / 512);
-  p.nsub = (T_ > 256 && nsub_env != 1 && 2 * pair_items > num_sms()) ? 2 : 1;
+  // ... unless the K loop is long enough that stream-K still gives every SM >= 40 k-blocks of
+  // paired tiles (13B T = 512: 5120 x 13824 fwd 675 -> 744 TFLOP/s, 5120 x 5120 stays single)
+  const bool long_k = (int64_t)pair_items * n_kblk >= 40LL * num_sms();
+  p.nsub = (T_ > 256 && nsub_env != 1 && (nsub_env == 2 || 2 * pair_items > num_sms() || long_k)) ? 2 : 1;
   p.bn = big ? 256 : 128;
   // CTA pairs (M = 256) for 256-token sub-tiles over an even number of m-blocks
   p.cg = (big && n_mblk % 2 == 0 && g_cg_mode == 2) ? 2 : 1;
@@ -1444,7 +1447,7 @@ int gemm_fwd(const qeft_linear_t* L, const void* x, int64_t ldx, void* y, int64_
   a.out_cols = L->oc;
   CUtensorMap m0, m1;
   const bool fast = (L->flags & QEFT_FLAG_STRUCTURED_FAST) && ldx % 8 == 0 && ((uintptr_t)x & 15) == 0;
-  const GemmPlan plan = gemm_plan(a.n_mblk, T_);
+  const GemmPlan plan = gemm_plan(a.n_mblk, T_, a.n_kblk);
   const int box = plan.bn / plan.cg;
   if (fast) {
     if (int r = make_map(&m0, x, L->act_dtype, L->m, T_, ldx, box)) return r;
@@ -1491,7 +1494,7 @@ int gemm_dgrad(const qeft_linear_t* L, const void* dy, int64_t lddy, void* dx, i
     a.accumulate = 0;
   }
   CUtensorMap m0;
-  const GemmPlan plan = gemm_plan(a.n_mblk, T_);
+  const GemmPlan plan = gemm_plan(a.n_mblk, T_, a.n_kblk);
   if (int r = make_map(&m0, dy, L->act_dtype, L->oc, T_, lddy, plan.bn / plan.cg)) return r;
   int r = L->act_dtype == QEFT_F16 ? dispatch_gemm<MODE_DGRAD, __half>(L, T_, plan, m0, m0, a, st)
                                    : dispatch_gemm<MODE_DGRAD, __nv_bfloat16>(L, T_, plan, m0, m0, a, st);
