@@ -156,3 +156,50 @@ def test_decode_attention_matches_rope_kv_sdpa(dt, B, pos):
     ulp = 2.0 ** -10 if dt == "f16" else 2.0 ** -7
     err = (o.float() - ref).abs().max()
     assert float(err) <= 2 * ulp * float(ref.abs().max()) + 1e-3, float(err)
+
+
+def test_residual_rms_norm_folds_the_residual_gradient(torch_):
+    """fused.residual_rms_norm: (x, norm(x)) whose backward is one rmsnorm_bwd with the
+    residual-path gradient folded in -- equal to rms_norm + an explicit residual add (fp32 sum
+    of the two fp16 terms rounded once vs twice: within one fp16 rounding)."""
+    torch = torch_
+    from paper_2410_08661_b200 import fused
+    x = torch.randn(2, 33, 4096, device="cuda").half().requires_grad_(True)
+    gain = 1.0 + 0.1 * torch.randn(4096, device="cuda")
+    d_res = torch.randn_like(x)
+    d_norm = torch.randn_like(x)
+    xp, y = fused.residual_rms_norm(x, gain)
+    assert xp.data_ptr() == x.data_ptr() and torch.equal(y, fused.rms_norm(x.detach(), gain))
+    torch.autograd.backward([xp, y], [d_res, d_norm])
+    x2 = x.detach().clone().requires_grad_(True)
+    torch.autograd.backward([x2, fused.rms_norm(x2, gain)], [d_res, d_norm])
+    scale = float(x2.grad.float().abs().max())
+    assert float((x.grad.float() - x2.grad.float()).abs().max()) <= 2 * 2.0 ** -10 * scale
+
+
+def test_grouped_linear_matches_separate_layers(torch_):
+    """qlinear.grouped_linear (q/k/v-style: one op, dX summed by the GEMM's reduce-add epilogue,
+    one dW launch) against the three QEFTLinear layers applied separately: same outputs, dX within
+    fp16 rounding of the summation order, dW_weak to fp32 summation order."""
+    torch = torch_
+    from paper_2410_08661_b200.decode import random_layer
+    from paper_2410_08661_b200.qlinear import QEFTLinear, grouped_linear
+    mods = [QEFTLinear(random_layer(oc, 1024, 128, 4, 128, "f16", seed=s), name=f"l{s}")
+            for s, oc in enumerate((512, 512, 256))]
+    x = torch.randn(300, 1024, device="cuda").half().requires_grad_(True)
+    dys = [torch.randn(300, m.oc, device="cuda").half() for m in mods]
+    ys = grouped_linear(mods, x)
+    torch.autograd.backward(ys, dys)
+    dx_g = x.grad.clone()
+    dw_g = [m.weak32.grad.clone() for m in mods]
+    for m in mods:
+        m.weak32.grad = None
+    x.grad = None
+    ys2 = [m(x) for m in mods]
+    for a_, b_ in zip(ys, ys2):
+        assert torch.equal(a_, b_)
+    torch.autograd.backward(ys2, dys)
+    scale = float(x.grad.float().abs().max())
+    assert float((dx_g.float() - x.grad.float()).abs().max()) <= 4 * 2.0 ** -10 * scale
+    for a_, m in zip(dw_g, mods):
+        assert rel_err(_np(a_), _np(m.weak32.grad)) <= 1e-5
