@@ -635,37 +635,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
   auto fslot = [&](int jq, int nst_r) {
     return CONTIG ? jq + warp_of_stage(jq * nst_r, nj * nst_r, NW) : jq * NW;
   };
-  for (int e = threadIdx.x; e < nj * redn; e += NW * 32) {
-    const int jq = e / redn, r = e - jq * redn;
-    if (CONTIG) {
-      const int wa = warp_of_stage(jq * nst, total, NW), wb = warp_of_stage(jq * nst + nst - 1, total, NW);
-      float* p = red + (size_t)jq * redn + r;
-      float v = 0.f;
-      for (int w = wa; w <= wb; ++w) v += p[w * redn];
-      p[wa * redn] = v;
-    } else {
-      float* p = red + (size_t)jq * NW * redn + r;
-      float v = 0.f;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) v += p[w * redn];
-      p[0] = v;
-    }
-  }
-  // ---- sum the S slices (ranks in order, over DSMEM) and store y ----
-  if (a.S > 1) cluster_sync();
-  else __syncthreads();
-  for (int e = threadIdx.x; e < nj * redn; e += NW * 32) {
-    const int jq = e / redn, r = e - jq * redn;
-    if (a.S > 1 && (jq % a.S) != rank) continue;
-    float v;
-    if (a.S > 1) {
-      // rank q's slot of row-block jq follows from its own slice geometry
-      v = 0.f;
-      for (int q = 0; q < a.S; ++q)
-        v += ld_dsmem_f32(smem_u32(red + (size_t)fslot(jq, a.geo[q].nst) * redn + r), q);
-    } else {
-      v = red[(size_t)fslot(jq, nst) * redn + r];
-    }
+  auto store = [&](int jq, int r, float v) {
     const int row16 = ONE ? r : r / n, col = ONE ? 0 : r - row16 * n;
     int lrb;
     const int l = layer_of(a, j0 + jq, lrb);
@@ -679,6 +649,38 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
         T* py = (T*)a.ys[l] + idx;
         *py = from_f32<T>((a.yflags & QEFT_Y_ACCUMULATE) ? to_f32<T>(*py) + v : v);
       }
+    }
+  };
+  // one K slice: the warp sum is the output (stored straight away, no second pass)
+  for (int e = threadIdx.x; e < nj * redn; e += NW * 32) {
+    const int jq = e / redn, r = e - jq * redn;
+    float v = 0.f;
+    float* dst;
+    if (CONTIG) {
+      const int wa = warp_of_stage(jq * nst, total, NW), wb = warp_of_stage(jq * nst + nst - 1, total, NW);
+      float* p = red + (size_t)jq * redn + r;
+      for (int w = wa; w <= wb; ++w) v += p[w * redn];
+      dst = p + wa * redn;
+    } else {
+      float* p = red + (size_t)jq * NW * redn + r;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) v += p[w * redn];
+      dst = p;
+    }
+    if (a.S > 1) *dst = v;
+    else store(jq, r, v);
+  }
+  // ---- K slices of a cluster: sum them (ranks in order, over DSMEM) and store y ----
+  if (a.S > 1) {
+    cluster_sync();
+    for (int e = threadIdx.x; e < nj * redn; e += NW * 32) {
+      const int jq = e / redn, r = e - jq * redn;
+      if ((jq % a.S) != rank) continue;
+      // rank q's slot of row-block jq follows from its own slice geometry
+      float v = 0.f;
+      for (int q = 0; q < a.S; ++q)
+        v += ld_dsmem_f32(smem_u32(red + (size_t)fslot(jq, a.geo[q].nst) * redn + r), q);
+      store(jq, r, v);
     }
   }
   if (a.S > 1) cluster_sync();  // keep this CTA's partials alive until every rank has read them
