@@ -230,8 +230,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
       }
   }
   if (tr && threadIdx.x == 0) tr[7] = gtime();
-  pdl_wait();
-  __syncthreads();  // xbar initialised before thread 0 arms it
+  pdl_wait();  // (xbar is initialised and armed by thread 0 itself; the others touch it only after
+               // the staging barrier below)
   if (tr && threadIdx.x == 0) tr[1] = gtime();
 
   // ---- stage x (B200 K order) for this CTA's K slice; zero the partials ----
