@@ -416,11 +416,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
   const uint32_t tmem = tmem_base;
 
   pdl_launch_dependents();
-  pdl_wait();  // activations come from the previous kernel
+  // The grid dependency is waited for by the roles that read what earlier kernels write: the TMA
+  // warp (activations, weak tiles), the epilogue (outputs) and the dequant producers after
+  // their first two k-blocks of codes -- the frozen codes and scales never change, so those
+  // loads overlap the previous kernel's tail.
   if (tr && threadIdx.x == 0) stamp(1);
 
   if (warp == 0) {
     // ================= TMA producer: activation tiles =================
+    pdl_wait();
     if (lane == 0) {
       int it = 0, ib = 0;
       for (int si = 0; si < plan.nseg; ++si) {
@@ -693,6 +697,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
       coords(1, mb, kb);
       load(mb, kb, P1);
     }
+    pdl_wait();
     for (int it = 0; it < total; ++it) {
       if (it + 2 < total) {
         int mb, kb;
@@ -743,6 +748,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_b0, const __grid_constant__ 
     }
   } else {
     // ================= epilogue: TMEM -> registers -> smem transpose -> global =================
+    pdl_wait();
     const int ew = warp - (2 + kProdWarps);
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     T* stg = sE + ew * 32 * kEpiStride;
