@@ -70,6 +70,10 @@ int gemv2_multi(const qeft_linear_t* const* Ls, int nl, const void* x, int64_t l
   a.yflags = y_f32;
   a.m = L->m;
   a.ic = L->ic;
+  // stages per warp L2-prefetched before the grid dependency (A/B on two boxes: stack +2 % /
+  // -0.3 %, decode step -1.6 % on both; 2 or 3 stages lose 4-7 %)
+  static const int l2pf = env_int("QEFT_GEMV2_L2PF", 1);
+  a.l2pf = l2pf;
   if (xu) {
     // fused SwiGLU: structured layers (x moved by bulk copies), 16-byte aligned rows
     if (!a.fast || (((uintptr_t)xu) & 15) != 0) return -1;

@@ -79,6 +79,7 @@ struct G2Args {
   int xs_ld;    // staged x row stride (elements)
   int64_t rbb;  // qweight bytes per row-block
   int ic;        // input columns (the raw x row staged for column-map gathers)
+  int l2pf;      // L2-prefetch each warp's first codes stage before the PDL wait
   const void* xu;      // fused SwiGLU input (model.py:389-391): x = silu(x) * xu (structured layers)
   int xu_off;          // byte offset of the staged xu rows in shared memory
   const float* ngain;  // fused RMS-norm of x (model.py:249-256): gain [ic] fp32, or null
@@ -231,6 +232,20 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv2_kernel(const G2Args a) {
   if constexpr (PRE > 0) {
     if (lane == 0)
       while (issued < PRE && issue(true)) {
+      }
+  } else {
+    // the first codes stage of this warp toward L2 (frozen data; the smem copy and the x copy
+    // are issued after the wait)
+    if (lane == 0)
+      for (int i = 0; i < a.l2pf && i < my_n; ++i) {
+        const int sidx = s_beg + i * sstep, jl_i = sidx / nst, t_i = sidx - jl_i * nst;
+        if (t_i >= ncs) continue;
+        int lrb;
+        const int l = layer_of(a, j0 + jl_i, lrb);
+        const int ca = sg.c0 + t_i * CPS, cb = min(ca + CPS, sg.c1);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a.qw[l] + lrb * a.rbb + ca * CB),
+                     "r"((uint32_t)(cb - ca) * CB)
+                     : "memory");
       }
   }
   if (tr && threadIdx.x == 0) tr[7] = gtime();
